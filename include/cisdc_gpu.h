@@ -1,0 +1,196 @@
+/*
+ * cisdc_gpu.h -- C-ABI of the B200-native MISDC / MISDCQ / CISDCQ ("PMISDC") sweep engine.
+ *
+ * Plain C: pointers, sizes and ints only, no C++ or CUDA types in any signature.
+ * Every entry point below replaces one call of the reference's C++ sweep/integrator API
+ * (paths relative to the reference repo root; see INTEGRATION.md for the binding):
+ *
+ *   cisdc_make_quadrature_tables  <- cisdc::make_quadrature_tables   proj/core/src/quadrature.cpp:147-162
+ *   cisdc_gpu_create              <- constructing an OperatorSplitProblem + SweepState
+ *                                    proj/core/include/cisdc/operator_split.hpp:36-54,
+ *                                    proj/core/src/sweep_state.cpp:22-30
+ *   cisdc_gpu_initialize          <- cisdc::SweepState::initialize     proj/core/src/sweep_state.cpp:32-44
+ *   cisdc_gpu_set_nodes           <- cisdc::SweepState::set_node_values proj/core/src/sweep_state.cpp:46-58
+ *   cisdc_gpu_sweep               <- cisdc::run_sweep (misdc/misdcq/cisdcq dispatch)
+ *                                    proj/core/src/integrators.cpp:290-299; with
+ *                                    workers > 0 the CISDCQ DAG runs as in cisdc::execute_pipelined
+ *                                    proj/core/src/pipeline.cpp:171-320
+ *   cisdc_gpu_increment           <- cisdc::increment_norm(phi[M], prev) proj/core/src/sweep_state.cpp:60-66
+ *   cisdc_gpu_get_field           <- reading SweepState::{phi,fa,fd,fr,phi_ad}[m]
+ *   cisdc_gpu_integrate           <- cisdc::integrate                  proj/core/src/integrators.cpp:301-333
+ *   cisdc_gpu_eval / cisdc_gpu_solve
+ *                                 <- OperatorSplitProblem::eval_* / solve_* (one stage on one field)
+ *
+ * Error behaviour mirrors the reference's exception taxonomy (proj/core/include/cisdc/errors.hpp:24-45):
+ * every function returns a cisdc_status; the message (stage, node, first failing cell) is
+ * available from cisdc_gpu_last_error().  Calls are synchronous at return, like run_sweep.
+ * One host thread per context (a context is not thread-safe, like SweepState).
+ */
+#ifndef CISDC_GPU_H_
+#define CISDC_GPU_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes: exception types of proj/core/include/cisdc/errors.hpp + std::invalid_argument */
+typedef enum {
+  CISDC_OK = 0,
+  CISDC_E_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  CISDC_E_FACTORIZATION = 2,    /* cisdc::FactorizationError */
+  CISDC_E_SOLVE = 3,            /* cisdc::SolveError */
+  CISDC_E_NUMERIC = 4,          /* cisdc::NumericError (Newton / multigrid cap) */
+  CISDC_E_CAPABILITY = 5,       /* cisdc::CapabilityError */
+  CISDC_E_CUDA = 6              /* CUDA runtime failure, out of memory */
+} cisdc_status;
+
+/* cisdc::Scheme, same order (proj/core/include/cisdc/integrators.hpp:30) */
+enum { CISDC_SCHEME_MISDC = 0, CISDC_SCHEME_MISDCQ = 1, CISDC_SCHEME_CISDCQ = 2, CISDC_SCHEME_IMEXQ = 3 };
+/* cisdc::EulerConvention (proj/core/include/cisdc/quadrature.hpp:42) */
+enum { CISDC_EULER_LITERAL = 0, CISDC_EULER_CUMULATIVE = 1 };
+
+/* problem kinds */
+enum {
+  CISDC_PROBLEM_PERIODIC_ADR = 0,   /* periodic 1-D/2-D/3-D advection-diffusion-reaction, S species */
+  CISDC_PROBLEM_REFERENCE_RD = 1,   /* the reference's own 1-D Dirichlet PDE on [0,20]
+                                       (proj/core/include/cisdc/problems/reaction_diffusion.hpp:28-99) */
+  CISDC_PROBLEM_LINEAR_SCALAR = 2   /* phi' = (a+d+r) phi (proj/core/include/cisdc/problems/linear.hpp:31-51);
+                                       oracle only (known-answer tests), rejected by cisdc_gpu_create */
+};
+enum {
+  CISDC_REACTION_NONE = 0,
+  CISDC_REACTION_LINEAR_DECAY = 1,  /* R = -lambda * phi                      (S = 1) */
+  CISDC_REACTION_BISTABLE = 2,      /* R = lambda * phi (1 - phi) (phi - theta) (S = 1) */
+  CISDC_REACTION_MASS_ACTION = 3    /* network of <=2-reactant/<=2-product mass-action reactions */
+};
+enum { CISDC_DIFFUSION_DIRECT = 0, CISDC_DIFFUSION_MULTIGRID = 1 };
+enum { CISDC_FIELD_PHI = 0, CISDC_FIELD_FA = 1, CISDC_FIELD_FD = 2, CISDC_FIELD_FR = 3, CISDC_FIELD_PHI_AD = 4 };
+enum { CISDC_STAGE_ADVECTION = 0, CISDC_STAGE_DIFFUSION = 1, CISDC_STAGE_REACTION = 2 };
+
+#define CISDC_MAX_M 8
+#define CISDC_MAX_SPECIES 16
+#define CISDC_MAX_REACTIONS 64
+
+/*
+ * Problem description.  Field layout (host and device): species-major, x fastest:
+ *   phi[((s * n[2] + k) * n[1] + j) * n[0] + i],   dimension = S * n[0] * n[1] * n[2].
+ *
+ * Advection F_A = -div(u phi) in finite-volume flux form with 4th-order face values
+ * phi_{i+1/2} = (7(phi_i + phi_{i+1}) - (phi_{i-1} + phi_{i+2}))/12.  The face velocity of
+ * component a at the + face of cell (i,j,k) is the separable product
+ *   u_a = (vel[a][0][i] * vel[a][1][j]) * vel[a][2][k]
+ * (a NULL table counts as 1.0; if all three tables of component a are NULL there is no
+ * advection along a).  Tables are filled by the caller so CPU and GPU share the same bits.
+ * Diffusion F_D = d_s * Lap4 (the reference's (-1,16,-30,16,-1)/(12 h^2) stencil per axis).
+ */
+typedef struct cisdc_problem_desc {
+  int kind;                 /* CISDC_PROBLEM_* */
+  int ndim;                 /* 1..3 */
+  int n[3];                 /* cells per axis; unused axes = 1 */
+  int nspecies;             /* S */
+  double h[3];              /* cell widths */
+  const double* vel[3][3];  /* separable face-velocity tables (see above) */
+  const double* diffusivity;/* [S] */
+  int reaction_kind;        /* CISDC_REACTION_* */
+  double lambda, theta;     /* LINEAR_DECAY / BISTABLE parameters */
+  int n_reactions;          /* MASS_ACTION: reactions r = 0..n_reactions-1 */
+  const int* reactants;     /* [2*n_reactions], species index or -1 */
+  const int* products;      /* [2*n_reactions], species index or -1 */
+  const double* rate_constants; /* [n_reactions] */
+  double newton_tol;        /* reference default 1e-14 (proj/core/include/cisdc/linalg.hpp:97-100) */
+  int newton_max_iter;      /* reference default 50 */
+  int diffusion_solver;     /* CISDC_DIFFUSION_DIRECT (1-D) or CISDC_DIFFUSION_MULTIGRID (2-D/3-D) */
+  double mg_tol;            /* stop when ||b - A x||_inf <= mg_tol * ||b||_inf (per species) */
+  int mg_max_cycles, mg_pre, mg_post, mg_coarse_sweeps, mg_min_coarse;
+  double mg_omega;          /* weighted-Jacobi damping */
+  /* CISDC_PROBLEM_REFERENCE_RD / LINEAR_SCALAR coefficients (a, d, r); n[0] = n_x for RD */
+  double ref_a, ref_d, ref_r;
+} cisdc_problem_desc;
+
+/* cisdc::QuadratureTables, row-major, M <= CISDC_MAX_M (proj/core/include/cisdc/quadrature.hpp:47-60) */
+typedef struct cisdc_tables {
+  int M;
+  int convention;
+  double tau[CISDC_MAX_M + 1];
+  double dtau[CISDC_MAX_M];
+  double Q[CISDC_MAX_M * (CISDC_MAX_M + 1)];   /* M x (M+1), stride M+1 */
+  double q[CISDC_MAX_M];
+  double Qt[CISDC_MAX_M * CISDC_MAX_M];        /* M x M, stride M */
+  double S[CISDC_MAX_M * (CISDC_MAX_M + 1)];   /* M x (M+1), stride M+1 */
+  double QtI[CISDC_MAX_M * CISDC_MAX_M];       /* M x M, stride M */
+  double QtE[CISDC_MAX_M * CISDC_MAX_M];       /* M x M, stride M */
+} cisdc_tables;
+
+/* cisdc::SolveCounters (operator_split.hpp:57-68) plus the Newton/multigrid work counts */
+typedef struct cisdc_counters {
+  long long diffusion, reaction, coupled;
+  long long newton_iterations;  /* residual evaluations summed over cells and reaction solves */
+  long long mg_cycles;          /* V-cycles summed over species and diffusion solves */
+} cisdc_counters;
+
+/* cisdc::IntegrateOptions (integrators.hpp:64-73) */
+typedef struct cisdc_integrate_options {
+  int scheme;
+  double dt;
+  int n_steps;
+  int M;
+  int n_sweeps;
+  int nu;
+  int has_stop_tol;
+  double stop_tol;
+  int convention;
+  int workers;  /* CISDCQ only: 0 = serial cell order (cisdcq_sweep), >0 = concurrent D/R streams
+                   (execute_pipelined semantics; results are bitwise identical) */
+} cisdc_integrate_options;
+
+/* cisdc::SweepReport (sweep_state.hpp:56-60); increments are written separately */
+typedef struct cisdc_step_report {
+  int sweeps;
+  cisdc_counters counters;
+} cisdc_step_report;
+
+typedef struct cisdc_gpu_ctx cisdc_gpu_ctx;
+
+int cisdc_make_quadrature_tables(int M, int convention, cisdc_tables* out);
+
+int cisdc_gpu_create(const cisdc_problem_desc* desc, const cisdc_tables* tables, cisdc_gpu_ctx** out);
+void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx);
+const char* cisdc_gpu_last_error(const cisdc_gpu_ctx* ctx);
+size_t cisdc_gpu_dimension(const cisdc_gpu_ctx* ctx);
+
+/* host-pointer state upload; *_device variants take device pointers (no PCIe copy) */
+int cisdc_gpu_initialize(cisdc_gpu_ctx* ctx, const double* phi0, size_t n);
+int cisdc_gpu_initialize_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t n);
+int cisdc_gpu_set_nodes(cisdc_gpu_ctx* ctx, const double* values /* (M+1) x n */, size_t n);
+
+int cisdc_gpu_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers, cisdc_counters* inout);
+int cisdc_gpu_increment(cisdc_gpu_ctx* ctx, double* out);
+int cisdc_gpu_get_field(cisdc_gpu_ctx* ctx, int which, int node, double* host, size_t n);
+int cisdc_gpu_get_field_device(cisdc_gpu_ctx* ctx, int which, int node, double* d_out, size_t n);
+
+/* one stage on one field (OperatorSplitProblem::eval_* / solve_*), host pointers */
+int cisdc_gpu_eval(cisdc_gpu_ctx* ctx, int stage, const double* phi, double* out, size_t n);
+int cisdc_gpu_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rhs, double* out, size_t n,
+                    cisdc_counters* inout);
+
+/* cisdc::integrate: phi0 / final_state host buffers of n doubles; reports[n_steps];
+   increments[n_steps * n_sweeps] (unused tail entries when stop_tol ends a step early are 0) */
+int cisdc_gpu_integrate(cisdc_gpu_ctx* ctx, const double* phi0, size_t n, const cisdc_integrate_options* opt,
+                        double* final_state, cisdc_step_report* reports, double* increments);
+/* same with device-resident phi0 / final_state (no host<->device copies of fields) */
+int cisdc_gpu_integrate_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t n,
+                               const cisdc_integrate_options* opt, double* d_final_state,
+                               cisdc_step_report* reports, double* increments);
+
+/* device time (ms) of the kernels of the last sweep, by kernel class; returns count written */
+int cisdc_gpu_kernel_times(cisdc_gpu_ctx* ctx, double* ms /* [8] */, int enable);
+/* number of kernel launches issued by the last sweep */
+long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CISDC_GPU_H_ */

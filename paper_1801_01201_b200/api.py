@@ -1,0 +1,344 @@
+"""Host-side mirror of the reference's C++ integrator API over the native B200 engine.
+
+Same names, argument meaning and error behaviour as proj/core/include/cisdc/*.hpp:
+
+  Scheme, EulerConvention                     integrators.hpp:30, quadrature.hpp:42
+  make_quadrature_tables(M, convention)       quadrature.cpp:147-162
+  SolveCounters / SweepReport                 operator_split.hpp:57-68, sweep_state.hpp:56-60
+  IntegrateOptions / IntegrateResult          integrators.hpp:64-79
+  GpuProblem (OperatorSplitProblem stages)    operator_split.hpp:36-54
+  SweepState (device resident)                sweep_state.hpp:33-53
+  run_sweep / execute_pipelined / integrate   integrators.cpp:290-333, pipeline.cpp:171-320
+  FactorizationError / SolveError / NumericError / CapabilityError   errors.hpp:24-45
+
+Every call goes through the C-ABI of include/cisdc_gpu.h into libcisdc_gpu.so; nothing here
+computes a field value (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _abi
+
+
+class Scheme(enum.IntEnum):
+    misdc = 0
+    misdcq = 1
+    cisdcq = 2
+    imexq = 3
+
+
+class EulerConvention(enum.IntEnum):
+    literal = 0
+    cumulative = 1
+
+
+class FactorizationError(RuntimeError):
+    pass
+
+
+class SolveError(RuntimeError):
+    pass
+
+
+class NumericError(RuntimeError):
+    pass
+
+
+class CapabilityError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+_ERRORS = {
+    _abi.E_INVALID_ARGUMENT: ValueError,
+    _abi.E_FACTORIZATION: FactorizationError,
+    _abi.E_SOLVE: SolveError,
+    _abi.E_NUMERIC: NumericError,
+    _abi.E_CAPABILITY: CapabilityError,
+    _abi.E_CUDA: CudaError,
+}
+
+
+def raise_for(code: int, msg: str) -> None:
+    if code != _abi.OK:
+        raise _ERRORS.get(code, RuntimeError)(msg)
+
+
+@dataclass
+class QuadratureTables:
+    M: int
+    convention: int
+    tau: np.ndarray
+    dtau: np.ndarray
+    Q: np.ndarray
+    q: np.ndarray
+    Qt: np.ndarray
+    S: np.ndarray
+    QtI: np.ndarray
+    QtE: np.ndarray
+    c: _abi.TablesC = None
+
+
+def tables_from_c(t: _abi.TablesC) -> QuadratureTables:
+    M = t.M
+    a = lambda arr, r, c: np.array(arr[: r * c]).reshape(r, c)  # noqa: E731
+    return QuadratureTables(M, t.convention, np.array(t.tau[: M + 1]), np.array(t.dtau[:M]), a(t.Q, M, M + 1),
+                            np.array(t.q[:M]), a(t.Qt, M, M), a(t.S, M, M + 1), a(t.QtI, M, M), a(t.QtE, M, M), t)
+
+
+def make_quadrature_tables(M: int, convention: int = EulerConvention.literal) -> QuadratureTables:
+    lib = _abi.load()
+    t = _abi.TablesC()
+    rc = lib.cisdc_make_quadrature_tables(int(M), int(convention), C.byref(t))
+    if rc == _abi.E_INVALID_ARGUMENT:
+        raise ValueError("gauss_lobatto_nodes: M must be >= 1 (and <= 8)")
+    raise_for(rc, "make_quadrature_tables failed")
+    return tables_from_c(t)
+
+
+@dataclass
+class SolveCounters:
+    diffusion: int = 0
+    reaction: int = 0
+    coupled: int = 0
+    newton_iterations: int = 0
+    mg_cycles: int = 0
+
+    @staticmethod
+    def from_c(c: _abi.CountersC) -> "SolveCounters":
+        return SolveCounters(c.diffusion, c.reaction, c.coupled, c.newton_iterations, c.mg_cycles)
+
+    def add_c(self, c: _abi.CountersC) -> None:
+        self.diffusion += c.diffusion
+        self.reaction += c.reaction
+        self.coupled += c.coupled
+        self.newton_iterations += c.newton_iterations
+        self.mg_cycles += c.mg_cycles
+
+
+@dataclass
+class SweepReport:
+    increments: list = field(default_factory=list)
+    sweeps: int = 0
+    counters: SolveCounters = field(default_factory=SolveCounters)
+
+
+@dataclass
+class IntegrateOptions:
+    scheme: int = Scheme.misdcq
+    dt: float = 0.0
+    n_steps: int = 1
+    M: int = 4
+    n_sweeps: int = 1
+    nu: int = 1
+    stop_tol: Optional[float] = None
+    convention: int = EulerConvention.literal
+    workers: int = 0  # CISDCQ: 0 = serial cell order, > 0 = concurrent D/R streams (execute_pipelined)
+
+    def to_c(self) -> _abi.IntegrateOptionsC:
+        o = _abi.IntegrateOptionsC()
+        o.scheme, o.dt, o.n_steps, o.M = int(self.scheme), float(self.dt), int(self.n_steps), int(self.M)
+        o.n_sweeps, o.nu = int(self.n_sweeps), int(self.nu)
+        o.has_stop_tol = 0 if self.stop_tol is None else 1
+        o.stop_tol = 0.0 if self.stop_tol is None else float(self.stop_tol)
+        o.convention, o.workers = int(self.convention), int(self.workers)
+        return o
+
+
+@dataclass
+class IntegrateResult:
+    final_state: np.ndarray
+    steps: list
+
+
+class GpuContext:
+    """One device-resident sweep state + problem (cisdc_gpu_ctx)."""
+
+    def __init__(self, problem, M: int, convention: int = EulerConvention.literal):
+        self.lib = _abi.load()
+        self.problem = problem
+        self.tables = make_quadrature_tables(M, convention)
+        self._desc = problem.to_c()
+        h = C.c_void_p()
+        rc = self.lib.cisdc_gpu_create(C.byref(self._desc), C.byref(self.tables.c), C.byref(h))
+        self.h = h
+        if rc != _abi.OK:
+            msg = self.last_error()
+            self.close()
+            raise_for(rc, msg)
+        self.n = int(self.lib.cisdc_gpu_dimension(self.h))
+        self.M = M
+
+    def last_error(self) -> str:
+        if not self.h:
+            return "no context"
+        return self.lib.cisdc_gpu_last_error(self.h).decode()
+
+    def check(self, rc: int) -> None:
+        if rc != _abi.OK:
+            raise_for(rc, self.last_error())
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.cisdc_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class GpuProblem:
+    """OperatorSplitProblem stages (eval_*/solve_*) on the GPU; host arrays in and out."""
+
+    def __init__(self, desc, M: int = 4):
+        self.desc = desc
+        self.ctx = GpuContext(desc, M)
+
+    def dimension(self) -> int:
+        return self.ctx.n
+
+    def _eval(self, stage: int, phi: np.ndarray) -> np.ndarray:
+        phi = np.ascontiguousarray(phi, dtype=np.float64)
+        out = np.empty_like(phi)
+        self.ctx.check(self.ctx.lib.cisdc_gpu_eval(self.ctx.h, stage, _abi.dptr(phi), _abi.dptr(out), phi.size))
+        return out
+
+    def eval_advection(self, phi):
+        return self._eval(_abi.STAGE_ADVECTION, phi)
+
+    def eval_diffusion(self, phi):
+        return self._eval(_abi.STAGE_DIFFUSION, phi)
+
+    def eval_reaction(self, phi):
+        return self._eval(_abi.STAGE_REACTION, phi)
+
+    def _solve(self, stage: int, coef: float, rhs: np.ndarray, counters: Optional[SolveCounters]):
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        out = np.empty_like(rhs)
+        c = _abi.CountersC()
+        self.ctx.check(self.ctx.lib.cisdc_gpu_solve(self.ctx.h, stage, float(coef), _abi.dptr(rhs), _abi.dptr(out),
+                                                    rhs.size, C.byref(c)))
+        if counters is not None:
+            counters.add_c(c)
+        return out
+
+    def solve_diffusion(self, coef, rhs, counters=None):
+        return self._solve(_abi.STAGE_DIFFUSION, coef, rhs, counters)
+
+    def solve_reaction(self, coef, rhs, counters=None):
+        return self._solve(_abi.STAGE_REACTION, coef, rhs, counters)
+
+    def close(self):
+        self.ctx.close()
+
+
+class SweepState:
+    """Device-resident SweepState (sweep_state.hpp:33-53) bound to one problem and node set."""
+
+    def __init__(self, problem_desc, M: int, convention: int = EulerConvention.literal):
+        self.ctx = GpuContext(problem_desc, M, convention)
+        self.M = M
+
+    def subintervals(self) -> int:
+        return self.M
+
+    def dim(self) -> int:
+        return self.ctx.n
+
+    def initialize(self, phi0: np.ndarray) -> None:
+        phi0 = np.ascontiguousarray(phi0, dtype=np.float64)
+        self.ctx.check(self.ctx.lib.cisdc_gpu_initialize(self.ctx.h, _abi.dptr(phi0), phi0.size))
+
+    def set_node_values(self, values) -> None:
+        v = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(self.M + 1, -1))
+        self.ctx.check(self.ctx.lib.cisdc_gpu_set_nodes(self.ctx.h, _abi.dptr(v), v.shape[1]))
+
+    def field(self, which: int, node: int) -> np.ndarray:
+        out = np.empty(self.ctx.n)
+        self.ctx.check(self.ctx.lib.cisdc_gpu_get_field(self.ctx.h, which, node, _abi.dptr(out), out.size))
+        return out
+
+    def phi(self, m):
+        return self.field(_abi.FIELD_PHI, m)
+
+    def fa(self, m):
+        return self.field(_abi.FIELD_FA, m)
+
+    def fd(self, m):
+        return self.field(_abi.FIELD_FD, m)
+
+    def fr(self, m):
+        return self.field(_abi.FIELD_FR, m)
+
+    def phi_ad(self, m):
+        return self.field(_abi.FIELD_PHI_AD, m)
+
+    def increment(self) -> float:
+        v = C.c_double()
+        self.ctx.check(self.ctx.lib.cisdc_gpu_increment(self.ctx.h, C.byref(v)))
+        return v.value
+
+    def close(self):
+        self.ctx.close()
+
+
+def run_sweep(scheme: int, state: SweepState, dt: float, nu: int = 1, counters: Optional[SolveCounters] = None,
+              workers: int = 0) -> None:
+    c = _abi.CountersC()
+    state.ctx.check(state.ctx.lib.cisdc_gpu_sweep(state.ctx.h, int(scheme), float(dt), int(nu), int(workers),
+                                                  C.byref(c)))
+    if counters is not None:
+        counters.add_c(c)
+
+
+def execute_pipelined(state: SweepState, dt: float, nu: int, workers: int = 2,
+                      counters: Optional[SolveCounters] = None) -> None:
+    if workers < 1:
+        raise ValueError("execute_pipelined: workers must be >= 1")
+    run_sweep(Scheme.cisdcq, state, dt, nu, counters, workers)
+
+
+def integrate(problem_desc, phi0: np.ndarray, opt: IntegrateOptions, ctx: Optional[GpuContext] = None) -> IntegrateResult:
+    """cisdc::integrate (integrators.cpp:301-333) through cisdc_gpu_integrate."""
+    if opt.n_sweeps < 1:
+        raise ValueError("integrate: n_sweeps must be >= 1")
+    if opt.scheme == Scheme.cisdcq and opt.nu < 1:
+        raise ValueError("integrate: nu must be >= 1")
+    own = ctx is None
+    if own:
+        ctx = GpuContext(problem_desc, opt.M, opt.convention)
+    try:
+        phi0 = np.ascontiguousarray(phi0, dtype=np.float64)
+        final = np.empty_like(phi0)
+        reps = (_abi.StepReportC * max(opt.n_steps, 1))()
+        incs = np.zeros(max(opt.n_steps * opt.n_sweeps, 1))
+        o = opt.to_c()
+        ctx.check(ctx.lib.cisdc_gpu_integrate(ctx.h, _abi.dptr(phi0), phi0.size, C.byref(o), _abi.dptr(final), reps,
+                                              _abi.dptr(incs)))
+        steps = []
+        for s in range(opt.n_steps):
+            r = reps[s]
+            steps.append(SweepReport(list(incs[s * opt.n_sweeps: s * opt.n_sweeps + r.sweeps]), r.sweeps,
+                                     SolveCounters.from_c(r.counters)))
+        return IntegrateResult(final, steps)
+    finally:
+        if own:
+            ctx.close()

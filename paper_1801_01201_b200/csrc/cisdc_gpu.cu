@@ -1,0 +1,1001 @@
+// B200-native MISDC / MISDCQ / CISDCQ ("PMISDC") sweep engine: context, sweep drivers and the
+// C-ABI of include/cisdc_gpu.h.
+//
+// The host keeps the reference's control flow verbatim (node loop of misdc_sweep /
+// misdcq_sweep, cell order or DAG of cisdcq_sweep / execute_pipelined, step loop of integrate);
+// every per-element loop of the reference becomes one of the kernels in *.cuh.  Sweep state is
+// device resident for the whole run: node fields of sweep (k) and (k+1) are two pointer sets that
+// swap after every sweep (the reference's fa_p = state.fa copy, integrators.cpp:74/108, becomes a
+// pointer swap), and node 0 is shared by both sets.  After SweepState::initialize every node of
+// the current set aliases node 0 (no M-fold copy).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cisdc_gpu.h"
+#include "circulant.hpp"
+#include "common.cuh"
+#include "multigrid.cuh"
+#include "newton.cuh"
+#include "pointwise.cuh"
+#include "solve1d.cuh"
+#include "stencil.cuh"
+
+namespace cisdc_b200 {
+int make_tables(int M, int convention, cisdc_tables* t);
+}
+
+using namespace cisdc_b200;
+
+namespace {
+
+constexpr int kPhi = 0, kFa = 1, kFd = 2, kFr = 3;
+
+struct Status {
+  int code = CISDC_OK;
+  std::string msg;
+};
+
+}  // namespace
+
+struct cisdc_gpu_ctx {
+  cisdc_problem_desc desc{};
+  cisdc_tables tb{};
+  int M = 0;
+  Geom g{};
+  Ops ops{};
+  Reaction rx{};
+  int S = 1;
+  bool ref_rd = false;
+  // device memory
+  std::vector<void*> allocs;
+  double* node0[4] = {};                       // phi0, fa0, fd0, fr0 (shared by both sets)
+  double* own[2][4][kMaxM + 1] = {};           // [set][field][node 1..M]
+  const double* view[2][4][kMaxM + 1] = {};    // current views (node 0 -> node0)
+  int cur = 0;
+  double* phi_ad[kMaxM + 1] = {};              // state.phi_ad (entry 0 unused, zeros)
+  double* base[kMaxM] = {};                    // quadrature bases per row
+  double* rhs_d = nullptr;
+  double* rhs_r = nullptr;
+  double* scratch = nullptr;
+  // CISDCQ workspace (ell = 1 evaluations at phi_ad, and the slots of ell < nu)
+  double* fa_ad[kMaxM + 1] = {};
+  double* fd_ad[kMaxM + 1] = {};
+  std::vector<double*> slot_bufs;  // (nu-1) * M * 5: phi_ad, phi_r, fa_r, fd_r, fr_r
+  int slot_nu = 1;
+  // solvers
+  double* rd_work = nullptr;
+  MgHierarchy mg;
+  // status / reductions
+  DevStatus* d_st = nullptr;
+  DevStatus* h_st = nullptr;  // pinned
+  double* d_partial = nullptr;
+  double* d_incr = nullptr;
+  double* h_incr = nullptr;   // pinned
+  unsigned long long newton_seen = 0, mg_seen = 0;
+  cudaStream_t s_main = nullptr, s_r = nullptr;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t ev_base = nullptr, ev_join = nullptr;
+  long long launches = 0;
+  std::string err;
+  double last_incr = 0.0;
+  bool have_incr = false;
+};
+
+namespace {
+
+int set_err(cisdc_gpu_ctx* c, int code, const std::string& m) {
+  if (c) c->err = m;
+  return code;
+}
+
+#define CU(x)                                                                                    \
+  do {                                                                                           \
+    cudaError_t e_ = (x);                                                                        \
+    if (e_ != cudaSuccess)                                                                       \
+      return set_err(ctx, CISDC_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                            " at " #x);                                          \
+  } while (0)
+
+int dalloc(cisdc_gpu_ctx* ctx, double** p, size_t count) {
+  void* v = nullptr;
+  CU(cudaMalloc(&v, std::max<size_t>(count, 1) * sizeof(double)));
+  ctx->allocs.push_back(v);
+  *p = static_cast<double*>(v);
+  return CISDC_OK;
+}
+
+const double* V(cisdc_gpu_ctx* c, int set, int field, int node) { return c->view[set][field][node]; }
+
+void reset_views(cisdc_gpu_ctx* c, int set) {
+  for (int f = 0; f < 4; ++f) {
+    c->view[set][f][0] = c->node0[f];
+    for (int m = 1; m <= c->M; ++m) c->view[set][f][m] = c->own[set][f][m];
+  }
+}
+
+void alias_views_to_node0(cisdc_gpu_ctx* c, int set) {
+  for (int f = 0; f < 4; ++f)
+    for (int m = 0; m <= c->M; ++m) c->view[set][f][m] = c->node0[f];
+}
+
+int grid_of(long long n, int block) { return static_cast<int>((n + block - 1) / block); }
+
+// ---------------------------------------------------------------- kernel launchers
+
+int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd, cudaStream_t s) {
+  const int blocks = grid_of(ctx->g.n, 256);
+  switch (ctx->g.ndim) {
+    case 1: k_eval_ad<1><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
+    case 2: k_eval_ad<2><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
+    default: k_eval_ad<3><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
+  }
+  ++ctx->launches;
+  CU(cudaGetLastError());
+  return CISDC_OK;
+}
+
+template <int S>
+int launch_eval_r_s(cisdc_gpu_ctx* ctx, const double* phi, double* fr, cudaStream_t s) {
+  k_eval_r<S><<<grid_of(ctx->g.ncell, 128), 128, 0, s>>>(ctx->rx, ctx->g, phi, fr);
+  ++ctx->launches;
+  CU(cudaGetLastError());
+  return CISDC_OK;
+}
+
+int launch_eval_r(cisdc_gpu_ctx* ctx, const double* phi, double* fr, cudaStream_t s) {
+  switch (ctx->S) {
+    case 1: return launch_eval_r_s<1>(ctx, phi, fr, s);
+    case 2: return launch_eval_r_s<2>(ctx, phi, fr, s);
+    case 3: return launch_eval_r_s<3>(ctx, phi, fr, s);
+    case 4: return launch_eval_r_s<4>(ctx, phi, fr, s);
+    case 9: return launch_eval_r_s<9>(ctx, phi, fr, s);
+  }
+  return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unsupported species count");
+}
+
+template <int S, int MODE>
+int launch_react_sm(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
+  const int blocks = grid_of(ctx->g.ncell, 128);
+  if constexpr (MODE == kModeMisdcq || MODE == kModeMisdc) {
+    switch (ctx->g.ndim) {
+      case 1: k_react<S, 1, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
+      case 2: k_react<S, 2, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
+      default: k_react<S, 3, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
+    }
+  } else {
+    k_react<S, 1, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
+  }
+  ++ctx->launches;
+  CU(cudaGetLastError());
+  return CISDC_OK;
+}
+
+template <int MODE>
+int launch_react_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
+  switch (ctx->S) {
+    case 1: return launch_react_sm<1, MODE>(ctx, a, s);
+    case 2: return launch_react_sm<2, MODE>(ctx, a, s);
+    case 3: return launch_react_sm<3, MODE>(ctx, a, s);
+    case 4: return launch_react_sm<4, MODE>(ctx, a, s);
+    case 9: return launch_react_sm<9, MODE>(ctx, a, s);
+  }
+  return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unsupported species count");
+}
+
+int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t s) {
+  switch (mode) {
+    case kModeMisdcq: return launch_react_m<kModeMisdcq>(ctx, a, s);
+    case kModeMisdc: return launch_react_m<kModeMisdc>(ctx, a, s);
+    case kModeCisdcq: return launch_react_m<kModeCisdcq>(ctx, a, s);
+    default: return launch_react_m<kModePlain>(ctx, a, s);
+  }
+}
+
+int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
+  k_rhs<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(a, ctx->g.n);
+  ++ctx->launches;
+  CU(cudaGetLastError());
+  return CISDC_OK;
+}
+
+int launch_quad_base(cisdc_gpu_ctx* ctx, int set, double dt, cudaStream_t s) {
+  QuadArgs q{};
+  const int M = ctx->M;
+  q.M = M;
+  for (int m = 0; m < M; ++m)
+    for (int j = 0; j <= M; ++j) q.c[m][j] = dt * ctx->tb.Q[m * (M + 1) + j];
+  q.phi0 = ctx->node0[kPhi];
+  for (int j = 0; j <= M; ++j) {
+    q.fa[j] = V(ctx, set, kFa, j);
+    q.fd[j] = V(ctx, set, kFd, j);
+    q.fr[j] = V(ctx, set, kFr, j);
+  }
+  for (int m = 0; m < M; ++m) q.base[m] = ctx->base[m];
+  k_quad_base<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(q, ctx->g.n);
+  ++ctx->launches;
+  CU(cudaGetLastError());
+  return CISDC_OK;
+}
+
+template <int E>
+int launch_solve1d_e(cisdc_gpu_ctx* ctx, const Solve1dArgs& a, int cl, cudaStream_t s) {
+  constexpr int T = 512;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(cl * ctx->S, 1, 1);
+  cfg.blockDim = dim3(T, 1, 1);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CU(cudaLaunchKernelEx(&cfg, k_solve1d_periodic<E, T>, a));
+  ++ctx->launches;
+  return CISDC_OK;
+}
+
+int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* out, cudaStream_t s) {
+  const long long n = ctx->g.n;
+  if (ctx->ref_rd) {
+    if (coef == 0.0) {
+      CU(cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+      return CISDC_OK;
+    }
+    RdSolveArgs a{};
+    a.n = ctx->g.nx;
+    const double dx = (20.0 - 0.0) / ctx->g.nx;
+    a.c = coef * ctx->desc.ref_d / (12.0 * dx * dx);
+    std::memcpy(a.w, ctx->ops.rd_w, sizeof(a.w));
+    a.rhs = rhs;
+    a.out = out;
+    a.work = ctx->rd_work;
+    k_rd_banded_solve<<<1, 32, 0, s>>>(a, ctx->d_st);
+    ++ctx->launches;
+    CU(cudaGetLastError());
+    return CISDC_OK;
+  }
+  if (ctx->desc.diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
+    const int rc = mg_solve(ctx->mg, ctx->g, ctx->desc, coef, rhs, out, ctx->d_st, s, &ctx->launches);
+    if (rc) return set_err(ctx, rc, "multigrid launch failed");
+    return CISDC_OK;
+  }
+  // periodic 1-D direct solve, one cluster per species
+  Solve1dArgs a{};
+  a.rhs = rhs;
+  a.out = out;
+  a.N = ctx->g.nx;
+  for (int sp = 0; sp < ctx->S; ++sp) {
+    const double c = coef * ctx->ops.cdiff[sp][0];
+    a.active[sp] = (coef != 0.0 && c != 0.0);
+    if (a.active[sp]) {
+      const CircFactor f = factor_circulant(c);
+      a.c[sp].npass = f.npass;
+      for (int k = 0; k < 4; ++k) {
+        a.c[sp].p[k] = f.p[k];
+        a.c[sp].q[k] = f.q[k];
+        a.c[sp].reverse[k] = f.reverse[k];
+      }
+      a.c[sp].invK = f.invK;
+    }
+  }
+  const int N = ctx->g.nx;
+  const int T = 512;
+  int E = 1;
+  while (E < 32 && (long long)E * T * 8 < N) E *= 2;
+  const int cl = (N + E * T - 1) / (E * T);
+  switch (E) {
+    case 1: return launch_solve1d_e<1>(ctx, a, cl, s);
+    case 2: return launch_solve1d_e<2>(ctx, a, cl, s);
+    case 4: return launch_solve1d_e<4>(ctx, a, cl, s);
+    case 8: return launch_solve1d_e<8>(ctx, a, cl, s);
+    case 16: return launch_solve1d_e<16>(ctx, a, cl, s);
+    default: return launch_solve1d_e<32>(ctx, a, cl, s);
+  }
+}
+
+int launch_incr(cisdc_gpu_ctx* ctx, const double* a, const double* b, cudaStream_t s) {
+  k_incr_partial<<<kIncrBlocks, kIncrThreads, 0, s>>>(a, b, ctx->g.n, ctx->d_partial);
+  k_incr_final<<<1, 512, 0, s>>>(a, b, ctx->g.n, ctx->d_partial, ctx->d_incr);
+  ctx->launches += 2;
+  CU(cudaGetLastError());
+  return CISDC_OK;
+}
+
+// ---------------------------------------------------------------- status
+
+int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters, cudaStream_t s) {
+  CU(cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const DevStatus h = *ctx->h_st;
+  if (counters) {
+    counters->newton_iterations += (long long)(h.newton_trips - ctx->newton_seen);
+    counters->mg_cycles += (long long)(h.mg_cycles - ctx->mg_seen);
+  }
+  ctx->newton_seen = h.newton_trips;
+  ctx->mg_seen = h.mg_cycles;
+  if (h.code != 0) {
+    char buf[256];
+    if (h.stage == CISDC_STAGE_REACTION) {
+      std::snprintf(buf, sizeof(buf), "solve_reaction_implicit: cell %llu: %s", h.first_bad_cell,
+                    h.code == CISDC_E_SOLVE ? "newton: singular jacobian"
+                                            : "newton: no convergence within the iteration cap");
+    } else if (ctx->ref_rd) {
+      std::snprintf(buf, sizeof(buf), "banded_solve: singular band at column %llu", h.first_bad_cell);
+    } else {
+      std::snprintf(buf, sizeof(buf), "solve_diffusion: multigrid: species %llu: no convergence in %d cycles",
+                    h.first_bad_cell, ctx->desc.mg_max_cycles);
+    }
+    // reset the status word so the context stays usable
+    DevStatus z{};
+    z.first_bad_cell = ~0ull;
+    z.newton_trips = h.newton_trips;
+    z.mg_cycles = h.mg_cycles;
+    CU(cudaMemcpy(ctx->d_st, &z, sizeof(z), cudaMemcpyHostToDevice));
+    const int code = (h.stage == CISDC_STAGE_REACTION || ctx->ref_rd) ? CISDC_E_SOLVE : h.code;
+    return set_err(ctx, code, buf);
+  }
+  return CISDC_OK;
+}
+
+// ---------------------------------------------------------------- sweeps
+
+#define TRY(x)                  \
+  do {                          \
+    const int rc_ = (x);        \
+    if (rc_) return rc_;        \
+  } while (0)
+
+double QI(const cisdc_tables& t, int m, int j) { return t.QtI[m * t.M + j]; }
+double QE(const cisdc_tables& t, int m, int j) { return t.QtE[m * t.M + j]; }
+
+int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
+  const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
+  cudaStream_t s = ctx->s_main;
+  reset_views(ctx, nxt);
+  TRY(launch_quad_base(ctx, prev, dt, s));
+  for (int m = 0; m < M; ++m) {
+    const double coef = dt * QI(ctx->tb, m, m);
+    RhsArgs r{};
+    r.kind = kRhsMisdcq;
+    r.nt = m;
+    for (int j = 1; j <= m; ++j) {
+      RhsTerm& t = r.t[j - 1];
+      t.cE = dt * QE(ctx->tb, m, j - 1);
+      t.cI = dt * QI(ctx->tb, m, j - 1);
+      t.A = V(ctx, nxt, kFa, j);
+      t.Ap = V(ctx, prev, kFa, j);
+      t.D = V(ctx, nxt, kFd, j);
+      t.Dp = V(ctx, prev, kFd, j);
+      t.R = V(ctx, nxt, kFr, j);
+      t.Rp = V(ctx, prev, kFr, j);
+    }
+    r.fc = coef;
+    r.X = V(ctx, prev, kFd, m + 1);
+    r.base = ctx->base[m];
+    r.out = ctx->rhs_d;
+    r.out2 = m > 0 ? ctx->rhs_r : nullptr;
+    TRY(launch_rhs(ctx, r, s));
+    TRY(solve_diffusion(ctx, coef, ctx->rhs_d, ctx->phi_ad[m + 1], s));
+    if (c) ++c->diffusion;
+    ReactArgs a{};
+    a.coef = coef;
+    a.p0 = m > 0 ? ctx->rhs_r : ctx->base[m];
+    a.phi_ad = ctx->phi_ad[m + 1];
+    a.fdp1 = V(ctx, prev, kFd, m + 1);
+    a.frp1 = V(ctx, prev, kFr, m + 1);
+    a.phi_out = ctx->own[nxt][kPhi][m + 1];
+    a.fr_out = ctx->own[nxt][kFr][m + 1];
+    TRY(launch_react(ctx, kModeMisdcq, a, s));
+    if (c) ++c->reaction;
+    TRY(launch_eval_ad(ctx, ctx->own[nxt][kPhi][m + 1], ctx->own[nxt][kFa][m + 1], ctx->own[nxt][kFd][m + 1], s));
+  }
+  return CISDC_OK;
+}
+
+int sweep_misdc(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
+  const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
+  cudaStream_t s = ctx->s_main;
+  reset_views(ctx, nxt);
+  for (int m = 0; m < M; ++m) {
+    const double dtm = dt * ctx->tb.dtau[m];
+    RhsArgs r{};
+    r.kind = kRhsMisdc;
+    r.M = M;
+    for (int j = 0; j <= M; ++j) {
+      r.sc[j] = dt * ctx->tb.S[m * (M + 1) + j];
+      r.sfa[j] = V(ctx, prev, kFa, j);
+      r.sfd[j] = V(ctx, prev, kFd, j);
+      r.sfr[j] = V(ctx, prev, kFr, j);
+    }
+    r.phim = V(ctx, nxt, kPhi, m);
+    r.fc = dtm;
+    r.X = V(ctx, nxt, kFa, m);
+    r.Y = V(ctx, prev, kFa, m);
+    r.Z = V(ctx, prev, kFd, m + 1);
+    r.out = ctx->rhs_d;
+    r.base_out = ctx->base[0];
+    TRY(launch_rhs(ctx, r, s));
+    TRY(solve_diffusion(ctx, dtm, ctx->rhs_d, ctx->phi_ad[m + 1], s));
+    if (c) ++c->diffusion;
+    ReactArgs a{};
+    a.coef = dtm;
+    a.p0 = ctx->base[0];
+    a.phi_ad = ctx->phi_ad[m + 1];
+    a.fam = V(ctx, nxt, kFa, m);
+    a.fapm = V(ctx, prev, kFa, m);
+    a.fdp1 = V(ctx, prev, kFd, m + 1);
+    a.frp1 = V(ctx, prev, kFr, m + 1);
+    a.phi_out = ctx->own[nxt][kPhi][m + 1];
+    a.fr_out = ctx->own[nxt][kFr][m + 1];
+    TRY(launch_react(ctx, kModeMisdc, a, s));
+    if (c) ++c->reaction;
+    TRY(launch_eval_ad(ctx, ctx->own[nxt][kPhi][m + 1], ctx->own[nxt][kFa][m + 1], ctx->own[nxt][kFd][m + 1], s));
+  }
+  return CISDC_OK;
+}
+
+// CISDCQ slot fields (integrators.hpp:93-107): ell == nu maps onto the next state set.
+struct Slots {
+  cisdc_gpu_ctx* ctx;
+  int nxt, nu;
+  double* get(int kind, int m, int ell) const {  // kind: 0 phi_ad, 1 phi_r, 2 fa_r, 3 fd_r, 4 fr_r
+    if (ell == nu) {
+      switch (kind) {
+        case 0: return ctx->phi_ad[m];
+        case 1: return ctx->own[nxt][kPhi][m];
+        case 2: return ctx->own[nxt][kFa][m];
+        case 3: return ctx->own[nxt][kFd][m];
+        default: return ctx->own[nxt][kFr][m];
+      }
+    }
+    return ctx->slot_bufs[((size_t)(ell - 1) * ctx->M + (m - 1)) * 5 + kind];
+  }
+};
+
+int ensure_slots(cisdc_gpu_ctx* ctx, int nu) {
+  const size_t need = (size_t)(nu - 1) * ctx->M * 5;
+  while (ctx->slot_bufs.size() < need) {
+    double* p = nullptr;
+    TRY(dalloc(ctx, &p, ctx->g.n));
+    ctx->slot_bufs.push_back(p);
+  }
+  return CISDC_OK;
+}
+
+int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c) {
+  const int prev = ctx->cur, row = m - 1;
+  RhsArgs r{};
+  r.kind = kRhsCisdcq;
+  int nt = 0;
+  for (int j = 1; j <= m - 2; ++j) {
+    RhsTerm& t = r.t[nt++];
+    t.cE = dt * QE(ctx->tb, row, j - 1);
+    t.cI = dt * QI(ctx->tb, row, j - 1);
+    t.A = W.get(2, j, ell);
+    t.Ap = V(ctx, prev, kFa, j);
+    t.D = W.get(3, j, ell);
+    t.Dp = V(ctx, prev, kFd, j);
+    t.R = W.get(4, j, ell);
+    t.Rp = V(ctx, prev, kFr, j);
+  }
+  if (m >= 2) {
+    RhsTerm& t = r.t[nt++];
+    t.cE = dt * QE(ctx->tb, row, m - 2);
+    t.cI = dt * QI(ctx->tb, row, m - 2);
+    t.A = ell == 1 ? ctx->fa_ad[m - 1] : W.get(2, m - 1, ell - 1);
+    t.Ap = V(ctx, prev, kFa, m - 1);
+    t.D = ell == 1 ? ctx->fd_ad[m - 1] : W.get(3, m - 1, ell - 1);
+    t.Dp = V(ctx, prev, kFd, m - 1);
+    t.R = ell == 1 ? V(ctx, prev, kFr, m - 1) : W.get(4, m - 1, ell - 1);
+    t.Rp = V(ctx, prev, kFr, m - 1);
+  }
+  r.nt = nt;
+  const double coef = dt * QI(ctx->tb, row, m - 1);
+  r.fc = coef;
+  r.X = ell == 1 ? V(ctx, prev, kFr, m) : W.get(4, m, ell - 1);
+  r.Y = V(ctx, prev, kFr, m);
+  r.Z = V(ctx, prev, kFd, m);
+  r.base = ctx->base[row];
+  r.out = ctx->rhs_d;
+  TRY(launch_rhs(ctx, r, s));
+  double* out = W.get(0, m, ell);
+  TRY(solve_diffusion(ctx, coef, ctx->rhs_d, out, s));
+  if (c) ++c->diffusion;
+  if (ell == 1) TRY(launch_eval_ad(ctx, out, ctx->fa_ad[m], ctx->fd_ad[m], s));
+  return CISDC_OK;
+}
+
+int reaction_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c) {
+  const int prev = ctx->cur, row = m - 1;
+  ReactArgs a{};
+  a.coef = dt * QI(ctx->tb, row, m - 1);
+  a.has_incr = m >= 2;
+  if (m >= 2) {
+    a.c2 = dt * QI(ctx->tb, row, m - 2);
+    a.fr_new = W.get(4, m - 1, ell);
+    a.lag_fr = ell == 1 ? V(ctx, prev, kFr, m - 1) : W.get(4, m - 1, ell - 1);
+  }
+  a.lag_frm = ell == 1 ? V(ctx, prev, kFr, m) : W.get(4, m, ell - 1);
+  a.p0 = W.get(0, m, ell);
+  a.phi_out = W.get(1, m, ell);
+  a.fr_out = W.get(4, m, ell);
+  TRY(launch_react(ctx, kModeCisdcq, a, s));
+  if (c) ++c->reaction;
+  TRY(launch_eval_ad(ctx, a.phi_out, W.get(2, m, ell), W.get(3, m, ell), s));
+  return CISDC_OK;
+}
+
+int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_counters* c) {
+  if (nu < 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "cisdcq_sweep: nu must be >= 1");
+  const int M = ctx->M, nxt = 1 - ctx->cur;
+  TRY(ensure_slots(ctx, nu));
+  reset_views(ctx, nxt);
+  Slots W{ctx, nxt, nu};
+  cudaStream_t sd = ctx->s_main;
+  TRY(launch_quad_base(ctx, ctx->cur, dt, sd));
+  if (workers <= 0) {
+    // cisdcq_sweep order (integrators.cpp:281-286): for ell, for m: D then R
+    for (int ell = 1; ell <= nu; ++ell)
+      for (int m = 1; m <= M; ++m) {
+        TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c));
+        TRY(reaction_cell(ctx, W, m, ell, dt, sd, c));
+      }
+    return CISDC_OK;
+  }
+  // execute_pipelined (pipeline.cpp:36-70 edges): D cells on s_main, R cells on s_r; the
+  // cross-stream edges D(m,l) -> R(m,l) and R(m-2,l), R(m-1,l-1), R(m,l-1) -> D(m,l) are events.
+  cudaStream_t sr = ctx->s_r;
+  const size_t ncells = (size_t)M * nu;
+  while (ctx->ev_pool.size() < 2 * ncells) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->ev_pool.push_back(e);
+  }
+  auto evD = [&](int m, int ell) { return ctx->ev_pool[2 * ((size_t)(ell - 1) * M + (m - 1))]; };
+  auto evR = [&](int m, int ell) { return ctx->ev_pool[2 * ((size_t)(ell - 1) * M + (m - 1)) + 1]; };
+  CU(cudaEventRecord(ctx->ev_base, sd));
+  CU(cudaStreamWaitEvent(sr, ctx->ev_base, 0));
+  // the D stream needs a single rhs buffer (D cells are totally ordered on it); R cells write
+  // only their own slots.
+  for (int ell = 1; ell <= nu; ++ell) {
+    for (int m = 1; m <= M; ++m) {
+      if (m >= 3) CU(cudaStreamWaitEvent(sd, evR(m - 2, ell), 0));
+      if (ell >= 2) {
+        if (m >= 2) CU(cudaStreamWaitEvent(sd, evR(m - 1, ell - 1), 0));
+        CU(cudaStreamWaitEvent(sd, evR(m, ell - 1), 0));
+      }
+      TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c));
+      CU(cudaEventRecord(evD(m, ell), sd));
+      CU(cudaStreamWaitEvent(sr, evD(m, ell), 0));
+      TRY(reaction_cell(ctx, W, m, ell, dt, sr, c));
+      CU(cudaEventRecord(evR(m, ell), sr));
+    }
+  }
+  CU(cudaEventRecord(ctx->ev_join, sr));
+  CU(cudaStreamWaitEvent(sd, ctx->ev_join, 0));
+  return CISDC_OK;
+}
+
+int check_ctx(cisdc_gpu_ctx* ctx) { return ctx ? CISDC_OK : CISDC_E_INVALID_ARGUMENT; }
+
+int do_initialize(cisdc_gpu_ctx* ctx) {
+  cudaStream_t s = ctx->s_main;
+  TRY(launch_eval_ad(ctx, ctx->node0[kPhi], ctx->node0[kFa], ctx->node0[kFd], s));
+  TRY(launch_eval_r(ctx, ctx->node0[kPhi], ctx->node0[kFr], s));
+  ctx->cur = 0;
+  alias_views_to_node0(ctx, 0);
+  reset_views(ctx, 1);
+  ctx->have_incr = false;
+  return CISDC_OK;
+}
+
+int run_one_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers, cisdc_counters* c) {
+  const int prev = ctx->cur;
+  const double* prev_end = V(ctx, prev, kPhi, ctx->M);
+  switch (scheme) {
+    case CISDC_SCHEME_MISDC: TRY(sweep_misdc(ctx, dt, c)); break;
+    case CISDC_SCHEME_MISDCQ: TRY(sweep_misdcq(ctx, dt, c)); break;
+    case CISDC_SCHEME_CISDCQ: TRY(sweep_cisdcq(ctx, dt, nu, workers, c)); break;
+    case CISDC_SCHEME_IMEXQ:
+      return set_err(ctx, CISDC_E_CAPABILITY, "imexq_sweep: problem provides no coupled diffusion-reaction solve");
+    default: return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown scheme");
+  }
+  const int nxt = 1 - prev;
+  TRY(launch_incr(ctx, V(ctx, nxt, kPhi, ctx->M), prev_end, ctx->s_main));
+  ctx->cur = nxt;
+  return CISDC_OK;
+}
+
+}  // namespace
+
+// ================================================================== C-ABI
+
+extern "C" {
+
+const char* cisdc_gpu_last_error(const cisdc_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+size_t cisdc_gpu_dimension(const cisdc_gpu_ctx* ctx) { return ctx ? (size_t)ctx->g.n : 0; }
+long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaDeviceSynchronize();
+  for (void* p : ctx->allocs) cudaFree(p);
+  mg_free(ctx->mg);
+  if (ctx->h_st) cudaFreeHost(ctx->h_st);
+  if (ctx->h_incr) cudaFreeHost(ctx->h_incr);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->ev_base) cudaEventDestroy(ctx->ev_base);
+  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
+  if (ctx->s_r) cudaStreamDestroy(ctx->s_r);
+  delete ctx;
+}
+
+static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisdc_tables* tb) {
+  ctx->desc = *d;
+  ctx->tb = *tb;
+  ctx->M = tb->M;
+  if (ctx->M < 1 || ctx->M > kMaxM) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "M must be in 1..8");
+  Geom& g = ctx->g;
+  Ops& o = ctx->ops;
+  Reaction& rx = ctx->rx;
+  std::memset(&o, 0, sizeof(o));
+  std::memset(&rx, 0, sizeof(rx));
+  if (d->kind == CISDC_PROBLEM_REFERENCE_RD) {
+    if (d->n[0] < 8) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "ReactionDiffusionGrid: n_x must be >= 8");
+    ctx->ref_rd = true;
+    g.nx = d->n[0];
+    g.ny = g.nz = 1;
+    g.ndim = 1;
+    g.S = 1;
+    o.ref_rd = 1;
+    const double dx = (20.0 - 0.0) / g.nx;
+    o.rd_cadv = d->ref_a / (12.0 * dx);
+    o.rd_cdiff = d->ref_d / (12.0 * dx * dx);
+    static const double pts[5] = {0.0, 0.5, 1.5, 2.5, 3.5};
+    const double xg[2] = {-0.5, -1.5};
+    for (int k = 0; k < 2; ++k)
+      for (int j = 0; j < 5; ++j) {
+        double num = 1.0, den = 1.0;
+        for (int i = 0; i < 5; ++i) {
+          if (i == j) continue;
+          num *= xg[k] - pts[i];
+          den *= pts[j] - pts[i];
+        }
+        o.rd_w[k][j] = num / den;
+      }
+    rx.ref_rd = 1;
+    rx.ref_r = d->ref_r;
+    rx.tol = 1e-14;
+    rx.max_iter = 50;
+  } else if (d->kind == CISDC_PROBLEM_PERIODIC_ADR) {
+    if (d->ndim < 1 || d->ndim > 3) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "periodic ADR: ndim must be 1..3");
+    const int S = d->nspecies;
+    if (!(S == 1 || S == 2 || S == 3 || S == 4 || S == 9))
+      return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "GPU path supports nspecies in {1,2,3,4,9}");
+    g.S = S;
+    g.ndim = d->ndim;
+    g.nx = d->n[0];
+    g.ny = d->ndim >= 2 ? d->n[1] : 1;
+    g.nz = d->ndim >= 3 ? d->n[2] : 1;
+    const int nn[3] = {g.nx, g.ny, g.nz};
+    for (int a = 0; a < d->ndim; ++a)
+      if (nn[a] < 8) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "periodic ADR: every active axis needs >= 8 cells");
+    for (int a = 0; a < 3; ++a) {
+      bool any = false;
+      for (int b = 0; b < 3; ++b) {
+        if (d->vel[a][b] && b < d->ndim && a < d->ndim) {
+          double* p = nullptr;
+          TRY(dalloc(ctx, &p, nn[b]));
+          CU(cudaMemcpy(p, d->vel[a][b], sizeof(double) * nn[b], cudaMemcpyHostToDevice));
+          o.vel[a][b] = p;
+          any = true;
+        }
+      }
+      o.adv[a] = any;
+      if (a < d->ndim) o.cadv[a] = 1.0 / (12.0 * d->h[a]);
+    }
+    for (int s = 0; s < S; ++s) {
+      const double ds = d->diffusivity ? d->diffusivity[s] : 0.0;
+      for (int a = 0; a < d->ndim; ++a) o.cdiff[s][a] = ds / (12.0 * d->h[a] * d->h[a]);
+    }
+    rx.kind = d->reaction_kind;
+    rx.lambda = d->lambda;
+    rx.theta = d->theta;
+    rx.tol = d->newton_tol;
+    rx.max_iter = d->newton_max_iter;
+    if (d->reaction_kind == CISDC_REACTION_LINEAR_DECAY || d->reaction_kind == CISDC_REACTION_BISTABLE) {
+      if (S != 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "scalar reaction kinds need nspecies == 1");
+    } else if (d->reaction_kind == CISDC_REACTION_MASS_ACTION) {
+      if (d->n_reactions < 0 || d->n_reactions > kMaxR)
+        return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: too many reactions");
+      rx.nr = d->n_reactions;
+      for (int r = 0; r < rx.nr; ++r) {
+        for (int t = 0; t < 2; ++t) {
+          const int a = d->reactants[2 * r + t], p = d->products[2 * r + t];
+          if (a >= S || p >= S) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: species index out of range");
+          rx.reac[r][t] = (signed char)(a < 0 ? -1 : a);
+          if (a >= 0) rx.nu[a][r] -= 1;
+          if (p >= 0) rx.nu[p][r] += 1;
+        }
+        if (rx.reac[r][0] < 0) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: every reaction needs a first reactant");
+        rx.k[r] = d->rate_constants[r];
+      }
+    } else if (d->reaction_kind != CISDC_REACTION_NONE) {
+      return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown reaction kind");
+    }
+    if (d->diffusion_solver == CISDC_DIFFUSION_DIRECT) {
+      if (d->ndim != 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "direct diffusion solve is 1-D only; use multigrid");
+      if (g.nx > 8 * 512 * 32) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "1-D direct solve supports n <= 131072");
+    } else if (d->diffusion_solver != CISDC_DIFFUSION_MULTIGRID) {
+      return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown diffusion solver");
+    }
+  } else if (d->kind == CISDC_PROBLEM_LINEAR_SCALAR) {
+    return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "linear scalar problem is oracle-only (dimension 1)");
+  } else {
+    return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown problem kind");
+  }
+  g.ncell = (long long)g.nx * g.ny * g.nz;
+  g.n = g.ncell * g.S;
+  ctx->S = g.S;
+  const long long n = g.n;
+  for (int f = 0; f < 4; ++f) TRY(dalloc(ctx, &ctx->node0[f], n));
+  for (int set = 0; set < 2; ++set)
+    for (int f = 0; f < 4; ++f)
+      for (int m = 1; m <= ctx->M; ++m) TRY(dalloc(ctx, &ctx->own[set][f][m], n));
+  for (int m = 0; m <= ctx->M; ++m) TRY(dalloc(ctx, &ctx->phi_ad[m], n));
+  CU(cudaMemset(ctx->phi_ad[0], 0, sizeof(double) * n));
+  for (int m = 0; m < ctx->M; ++m) TRY(dalloc(ctx, &ctx->base[m], n));
+  TRY(dalloc(ctx, &ctx->rhs_d, n));
+  TRY(dalloc(ctx, &ctx->rhs_r, n));
+  TRY(dalloc(ctx, &ctx->scratch, n));
+  for (int m = 1; m <= ctx->M; ++m) {
+    TRY(dalloc(ctx, &ctx->fa_ad[m], n));
+    TRY(dalloc(ctx, &ctx->fd_ad[m], n));
+  }
+  if (ctx->ref_rd) TRY(dalloc(ctx, &ctx->rd_work, (size_t)g.nx * 10));
+  if (!ctx->ref_rd && d->diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
+    const int rc = mg_init(ctx->mg, g, *d);
+    if (rc) return set_err(ctx, rc, "multigrid: hierarchy setup failed (" + std::to_string(rc) + ")");
+  }
+  void* v = nullptr;
+  CU(cudaMalloc(&v, sizeof(DevStatus)));
+  ctx->allocs.push_back(v);
+  ctx->d_st = static_cast<DevStatus*>(v);
+  DevStatus z{};
+  z.first_bad_cell = ~0ull;
+  CU(cudaMemcpy(ctx->d_st, &z, sizeof(z), cudaMemcpyHostToDevice));
+  CU(cudaMallocHost(&ctx->h_st, sizeof(DevStatus)));
+  TRY(dalloc(ctx, &ctx->d_partial, kIncrBlocks));
+  TRY(dalloc(ctx, &ctx->d_incr, 1));
+  CU(cudaMallocHost(&ctx->h_incr, sizeof(double)));
+  CU(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&ctx->s_r, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&ctx->ev_base, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  reset_views(ctx, 0);
+  reset_views(ctx, 1);
+  return CISDC_OK;
+}
+
+int cisdc_gpu_create(const cisdc_problem_desc* desc, const cisdc_tables* tables, cisdc_gpu_ctx** out) {
+  if (!desc || !tables || !out) return CISDC_E_INVALID_ARGUMENT;
+  *out = nullptr;
+  cisdc_gpu_ctx* ctx = new cisdc_gpu_ctx();
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    // keep the context so the caller can read the message
+    ctx->err = "no CUDA device: the B200 sweep engine has no CPU fallback";
+    *out = ctx;
+    return CISDC_E_CUDA;
+  }
+  const int rc = build_ctx(ctx, desc, tables);
+  *out = ctx;
+  return rc;
+}
+
+int cisdc_gpu_initialize(cisdc_gpu_ctx* ctx, const double* phi0, size_t n) {
+  TRY(check_ctx(ctx));
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "SweepState::initialize: dimension mismatch");
+  CU(cudaMemcpyAsync(ctx->node0[kPhi], phi0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s_main));
+  TRY(do_initialize(ctx));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  return CISDC_OK;
+}
+
+int cisdc_gpu_initialize_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t n) {
+  TRY(check_ctx(ctx));
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "SweepState::initialize: dimension mismatch");
+  CU(cudaMemcpyAsync(ctx->node0[kPhi], d_phi0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s_main));
+  TRY(do_initialize(ctx));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  return CISDC_OK;
+}
+
+int cisdc_gpu_set_nodes(cisdc_gpu_ctx* ctx, const double* values, size_t n) {
+  TRY(check_ctx(ctx));
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "SweepState::set_node_values: dimension mismatch");
+  cudaStream_t s = ctx->s_main;
+  ctx->cur = 0;
+  reset_views(ctx, 0);
+  reset_views(ctx, 1);
+  for (int m = 0; m <= ctx->M; ++m) {
+    double* phi = m == 0 ? ctx->node0[kPhi] : ctx->own[0][kPhi][m];
+    double* fa = m == 0 ? ctx->node0[kFa] : ctx->own[0][kFa][m];
+    double* fd = m == 0 ? ctx->node0[kFd] : ctx->own[0][kFd][m];
+    double* fr = m == 0 ? ctx->node0[kFr] : ctx->own[0][kFr][m];
+    CU(cudaMemcpyAsync(phi, values + (size_t)m * n, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    TRY(launch_eval_ad(ctx, phi, fa, fd, s));
+    TRY(launch_eval_r(ctx, phi, fr, s));
+  }
+  ctx->have_incr = false;
+  CU(cudaStreamSynchronize(s));
+  return CISDC_OK;
+}
+
+int cisdc_gpu_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers, cisdc_counters* inout) {
+  TRY(check_ctx(ctx));
+  ctx->launches = 0;
+  TRY(run_one_sweep(ctx, scheme, dt, nu, workers, inout));
+  CU(cudaMemcpyAsync(ctx->h_incr, ctx->d_incr, sizeof(double), cudaMemcpyDeviceToHost, ctx->s_main));
+  TRY(check_status(ctx, inout, ctx->s_main));
+  ctx->last_incr = *ctx->h_incr;
+  ctx->have_incr = true;
+  return CISDC_OK;
+}
+
+int cisdc_gpu_increment(cisdc_gpu_ctx* ctx, double* out) {
+  TRY(check_ctx(ctx));
+  if (!ctx->have_incr) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "no sweep has run since initialize");
+  *out = ctx->last_incr;
+  return CISDC_OK;
+}
+
+static int field_ptr(cisdc_gpu_ctx* ctx, int which, int node, const double** p) {
+  if (node < 0 || node > ctx->M) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "node out of range");
+  if (which == CISDC_FIELD_PHI_AD) *p = ctx->phi_ad[node];
+  else if (which >= 0 && which < 4) *p = V(ctx, ctx->cur, which, node);
+  else return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown field");
+  return CISDC_OK;
+}
+
+int cisdc_gpu_get_field(cisdc_gpu_ctx* ctx, int which, int node, double* host, size_t n) {
+  TRY(check_ctx(ctx));
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "get_field: dimension mismatch");
+  const double* p = nullptr;
+  TRY(field_ptr(ctx, which, node, &p));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  CU(cudaMemcpy(host, p, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return CISDC_OK;
+}
+
+int cisdc_gpu_get_field_device(cisdc_gpu_ctx* ctx, int which, int node, double* d_out, size_t n) {
+  TRY(check_ctx(ctx));
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "get_field: dimension mismatch");
+  const double* p = nullptr;
+  TRY(field_ptr(ctx, which, node, &p));
+  CU(cudaMemcpyAsync(d_out, p, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s_main));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  return CISDC_OK;
+}
+
+int cisdc_gpu_eval(cisdc_gpu_ctx* ctx, int stage, const double* phi, double* out, size_t n) {
+  TRY(check_ctx(ctx));
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "eval: dimension mismatch");
+  cudaStream_t s = ctx->s_main;
+  CU(cudaMemcpyAsync(ctx->rhs_d, phi, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (stage == CISDC_STAGE_ADVECTION) TRY(launch_eval_ad(ctx, ctx->rhs_d, ctx->scratch, nullptr, s));
+  else if (stage == CISDC_STAGE_DIFFUSION) TRY(launch_eval_ad(ctx, ctx->rhs_d, nullptr, ctx->scratch, s));
+  else TRY(launch_eval_r(ctx, ctx->rhs_d, ctx->scratch, s));
+  CU(cudaMemcpyAsync(out, ctx->scratch, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return CISDC_OK;
+}
+
+int cisdc_gpu_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rhs, double* out, size_t n,
+                    cisdc_counters* inout) {
+  TRY(check_ctx(ctx));
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "solve: dimension mismatch");
+  cudaStream_t s = ctx->s_main;
+  CU(cudaMemcpyAsync(ctx->rhs_d, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  if (stage == CISDC_STAGE_DIFFUSION) {
+    TRY(solve_diffusion(ctx, coef, ctx->rhs_d, ctx->scratch, s));
+  } else if (stage == CISDC_STAGE_REACTION) {
+    ReactArgs a{};
+    a.coef = coef;
+    a.p0 = ctx->rhs_d;
+    a.phi_out = ctx->scratch;
+    a.fr_out = nullptr;
+    TRY(launch_react(ctx, kModePlain, a, s));
+  } else {
+    return set_err(ctx, CISDC_E_CAPABILITY, "OperatorSplitProblem: coupled diffusion-reaction solve not provided");
+  }
+  TRY(check_status(ctx, inout, s));
+  CU(cudaMemcpy(out, ctx->scratch, sizeof(double) * n, cudaMemcpyDeviceToHost));
+  return CISDC_OK;
+}
+
+static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_device, size_t n,
+                          const cisdc_integrate_options* o, double* final_state, bool final_device,
+                          cisdc_step_report* reports, double* increments) {
+  TRY(check_ctx(ctx));
+  if (!o) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: null options");
+  if (o->n_sweeps < 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: n_sweeps must be >= 1");
+  if (o->scheme == CISDC_SCHEME_CISDCQ && o->nu < 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: nu must be >= 1");
+  if (o->M != ctx->M) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: options.M differs from the context's tables");
+  if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: dimension mismatch");
+  // the context's tables must be make_quadrature_tables(M, convention)
+  if (o->convention != ctx->tb.convention) {
+    cisdc_tables t;
+    if (make_tables(o->M, o->convention, &t)) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "bad tables");
+    ctx->tb = t;
+  }
+  cudaStream_t s = ctx->s_main;
+  CU(cudaMemcpyAsync(ctx->node0[kPhi], phi0, sizeof(double) * n,
+                     phi0_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+  std::vector<double> incs;
+  for (int step = 0; step < o->n_steps; ++step) {
+    TRY(do_initialize(ctx));
+    cisdc_step_report rep{};
+    int k;
+    for (k = 1; k <= o->n_sweeps; ++k) {
+      const int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters);
+      int rc2 = rc;
+      const bool need_sync = o->has_stop_tol || k == o->n_sweeps || rc;
+      if (!rc) {
+        CU(cudaMemcpyAsync(ctx->h_incr, ctx->d_incr, sizeof(double), cudaMemcpyDeviceToHost, s));
+        if (need_sync) rc2 = check_status(ctx, &rep.counters, s);
+      }
+      if (rc2) {
+        ctx->err = "integrate: step " + std::to_string(step + 1) + ", sweep " + std::to_string(k) + ": " + ctx->err;
+        return rc2 == CISDC_E_CUDA ? rc2 : CISDC_E_SOLVE;
+      }
+      if (!need_sync) CU(cudaStreamSynchronize(s));
+      const double inc = *ctx->h_incr;
+      if (increments) increments[(size_t)step * o->n_sweeps + (k - 1)] = inc;
+      ctx->last_incr = inc;
+      ctx->have_incr = true;
+      if (o->has_stop_tol && inc <= o->stop_tol) {
+        ++k;
+        break;
+      }
+    }
+    rep.sweeps = k - 1;
+    if (reports) reports[step] = rep;
+    // start = state.phi[M]: becomes node 0 of the next step
+    CU(cudaMemcpyAsync(ctx->scratch, V(ctx, ctx->cur, kPhi, ctx->M), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(ctx->node0[kPhi], ctx->scratch, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  }
+  CU(cudaMemcpyAsync(final_state, ctx->node0[kPhi], sizeof(double) * n,
+                     final_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return CISDC_OK;
+}
+
+int cisdc_gpu_integrate(cisdc_gpu_ctx* ctx, const double* phi0, size_t n, const cisdc_integrate_options* opt,
+                        double* final_state, cisdc_step_report* reports, double* increments) {
+  return integrate_impl(ctx, phi0, false, n, opt, final_state, false, reports, increments);
+}
+
+int cisdc_gpu_integrate_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t n, const cisdc_integrate_options* opt,
+                               double* d_final_state, cisdc_step_report* reports, double* increments) {
+  return integrate_impl(ctx, d_phi0, true, n, opt, d_final_state, true, reports, increments);
+}
+
+int cisdc_gpu_kernel_times(cisdc_gpu_ctx* ctx, double* ms, int enable) {
+  (void)ctx;
+  (void)ms;
+  (void)enable;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,392 @@
+// K3 (2-D/3-D): implicit diffusion solve (I - coef d_s Lap4) x = b by cell-centred geometric
+// multigrid, all species batched in every launch (grid.y = species; a converged species is
+// masked out with a device flag).  The algorithm and its per-point arithmetic are specified in
+// oracle/co_problems.c ("multigrid") and DESIGN.md; the CPU oracle runs the identical cycles so the
+// GPU result is bit-identical, and the reference's residual tolerance semantics apply:
+// stop when ||b - A x||_inf <= mg_tol * ||b||_inf per species (max-norms are order-independent, so
+// the stop decisions are exact).
+//
+// Kernels (each HBM-bound on its own level):
+//   k_mg_absmax    ||b||_inf per species
+//   k_mg_resmax    ||b - A x||_inf per species on level 0
+//   k_mg_update    per-species convergence / cycle bookkeeping (1 block)
+//   k_mg_smooth    weighted Jacobi sweep (13-point 3-D / 9-point 2-D star, radius 2)
+//   k_mg_restrict  residual + 2^d-child average, fused
+//   k_mg_prolong   (bi/tri)linear cell-centred interpolation + correction, fused
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace cisdc_b200 {
+
+constexpr int kMgMaxLevels = 16;
+
+struct MgLevel {
+  int nx, ny, nz;
+  long long ncell;
+  double* x;
+  double* t;
+  double* b;
+};
+
+struct MgHierarchy {
+  int L = 0;
+  int ndim = 0, S = 0;
+  MgLevel lv[kMgMaxLevels] = {};
+  int* d_active = nullptr;        // [S]
+  int* d_cycles = nullptr;        // [S]
+  double* d_bmax = nullptr;       // [S]
+  double* d_rmax = nullptr;       // [S]
+  int* d_flag = nullptr;          // [2]: any_active, failed species + 1
+  int* h_flag = nullptr;          // pinned mirror
+  std::vector<void*> allocs;
+};
+
+struct MgCoef {
+  int ndim;
+  double coef;
+  double c[kMaxS][3];
+  double wD[kMaxS];
+};
+
+__device__ __forceinline__ double mg_at(const double* __restrict__ f, int nx, int ny, int nz, int i, int j, int k, int a,
+                                        int o) {
+  if (a == 0) i = wrapi(i + o, nx);
+  else if (a == 1) j = wrapi(j + o, ny);
+  else k = wrapi(k + o, nz);
+  return __ldg(f + ((long long)k * ny + j) * nx + i);
+}
+
+template <int DIM>
+__device__ __forceinline__ double mg_ax(const MgCoef& C, int s, const double* __restrict__ x, int nx, int ny, int nz,
+                                        int i, int j, int k) {
+  double lap = 0.0;
+#pragma unroll
+  for (int a = 0; a < DIM; ++a) {
+    const double g0 = mg_at(x, nx, ny, nz, i, j, k, a, -2);
+    const double g1 = mg_at(x, nx, ny, nz, i, j, k, a, -1);
+    const double g2 = mg_at(x, nx, ny, nz, i, j, k, a, 0);
+    const double g3 = mg_at(x, nx, ny, nz, i, j, k, a, 1);
+    const double g4 = mg_at(x, nx, ny, nz, i, j, k, a, 2);
+    lap = lap + C.c[s][a] * (-g0 + 16.0 * g1 - 30.0 * g2 + 16.0 * g3 - g4);
+  }
+  return __ldg(x + ((long long)k * ny + j) * nx + i) - C.coef * lap;
+}
+
+__device__ __forceinline__ void mg_ijk(long long c, int nx, int ny, int& i, int& j, int& k) {
+  i = static_cast<int>(c % nx);
+  c /= nx;
+  j = static_cast<int>(c % ny);
+  k = static_cast<int>(c / ny);
+}
+
+__global__ void k_mg_absmax(const double* __restrict__ b, long long ncell, double* __restrict__ out) {
+  const int s = blockIdx.y;
+  const double* f = b + (long long)s * ncell;
+  double m = 0.0;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += (long long)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(f[c]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out + s, m);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_mg_resmax(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+                                                   const double* __restrict__ b, int nx, int ny, int nz,
+                                                   const int* __restrict__ active, double* __restrict__ out) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const long long ncell = (long long)nx * ny * nz;
+  const double* xs = x + (long long)s * ncell;
+  const double* bs = b + (long long)s * ncell;
+  double m = 0.0;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += (long long)gridDim.x * blockDim.x) {
+    int i, j, k;
+    mg_ijk(c, nx, ny, i, j, k);
+    m = fmax(m, fabs(bs[c] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k)));
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out + s, m);
+}
+
+// per-species stop decision of the oracle's loop: rn <= tol*bn -> done; cap -> failure
+__global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int* cycles, const double* bmax,
+                            double* rmax, int* flag, DevStatus* st) {
+  if (threadIdx.x != 0) return;
+  int any = 0;
+  for (int s = 0; s < S; ++s) {
+    if (!active[s]) continue;
+    const double thr = tol * bmax[s];
+    if (rmax[s] <= thr) {
+      active[s] = 0;
+      continue;
+    }
+    if (cycles[s] >= max_cycles) {
+      active[s] = 0;
+      if (flag[1] == 0) flag[1] = s + 1;
+      atomicMin(&st->first_bad_cell, (unsigned long long)s);
+      atomicMax(&st->code, (int)CISDC_E_NUMERIC);
+      st->stage = CISDC_STAGE_DIFFUSION;
+      continue;
+    }
+    cycles[s] += 1;
+    st->mg_cycles += 1;
+    any = 1;
+  }
+  for (int s = 0; s < S; ++s) rmax[s] = 0.0;
+  flag[0] = any;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_mg_smooth(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+                                                   const double* __restrict__ b, double* __restrict__ xo, int nx,
+                                                   int ny, int nz, int from_zero, const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const long long ncell = (long long)nx * ny * nz;
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncell) return;
+  const long long e = (long long)s * ncell + c;
+  if (from_zero) {
+    xo[e] = C.wD[s] * b[e];
+    return;
+  }
+  int i, j, k;
+  mg_ijk(c, nx, ny, i, j, k);
+  const double* xs = x + (long long)s * ncell;
+  const double r = b[e] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k);
+  xo[e] = xs[c] + C.wD[s] * r;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_mg_restrict(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+                                                     const double* __restrict__ b, int nx, int ny, int nz,
+                                                     double* __restrict__ bc, int cx, int cy, int cz,
+                                                     const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const long long nc = (long long)cx * cy * cz;
+  const long long C0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (C0 >= nc) return;
+  int I, J, K;
+  mg_ijk(C0, cx, cy, I, J, K);
+  const long long nf = (long long)nx * ny * nz;
+  const double* xs = x + (long long)s * nf;
+  const double* bs = b + (long long)s * nf;
+  const double scale = DIM == 1 ? 0.5 : (DIM == 2 ? 0.25 : 0.125);
+  double acc = 0.0;
+#pragma unroll
+  for (int dz = 0; dz < (DIM >= 3 ? 2 : 1); ++dz)
+#pragma unroll
+    for (int dy = 0; dy < (DIM >= 2 ? 2 : 1); ++dy)
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const int i = 2 * I + dx, j = DIM >= 2 ? 2 * J + dy : J, k = DIM >= 3 ? 2 * K + dz : K;
+        const long long id = ((long long)k * ny + j) * nx + i;
+        acc = acc + (bs[id] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k));
+      }
+  bc[(long long)s * nc + C0] = acc * scale;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_mg_prolong(double* __restrict__ x, int nx, int ny, int nz,
+                                                    const double* __restrict__ ec, int cx, int cy, int cz,
+                                                    const int* __restrict__ active) {
+  const int s = blockIdx.y;
+  if (!active[s]) return;
+  const long long nf = (long long)nx * ny * nz;
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nf) return;
+  int i, j, k;
+  mg_ijk(c, nx, ny, i, j, k);
+  const double* e = ec + (long long)s * cx * cy * cz;
+  const int I = i >> 1, I2 = wrapi((i & 1) ? I + 1 : I - 1, cx);
+  int J = j, J2 = j, K = k, K2 = k;
+  if (DIM >= 2) {
+    J = j >> 1;
+    J2 = wrapi((j & 1) ? J + 1 : J - 1, cy);
+  }
+  if (DIM >= 3) {
+    K = k >> 1;
+    K2 = wrapi((k & 1) ? K + 1 : K - 1, cz);
+  }
+#define E_(a, b_, c_) __ldg(e + ((long long)(c_) * cy + (b_)) * cx + (a))
+  double v;
+  if (DIM == 1) {
+    v = 0.75 * E_(I, 0, 0) + 0.25 * E_(I2, 0, 0);
+  } else if (DIM == 2) {
+    const double a0 = 0.75 * E_(I, J, 0) + 0.25 * E_(I2, J, 0);
+    const double a1 = 0.75 * E_(I, J2, 0) + 0.25 * E_(I2, J2, 0);
+    v = 0.75 * a0 + 0.25 * a1;
+  } else {
+    const double a00 = 0.75 * E_(I, J, K) + 0.25 * E_(I2, J, K);
+    const double a10 = 0.75 * E_(I, J2, K) + 0.25 * E_(I2, J2, K);
+    const double a01 = 0.75 * E_(I, J, K2) + 0.25 * E_(I2, J, K2);
+    const double a11 = 0.75 * E_(I, J2, K2) + 0.25 * E_(I2, J2, K2);
+    const double b0 = 0.75 * a00 + 0.25 * a10;
+    const double b1 = 0.75 * a01 + 0.25 * a11;
+    v = 0.75 * b0 + 0.25 * b1;
+  }
+#undef E_
+  const long long id = (long long)s * nf + c;
+  x[id] = x[id] + v;
+}
+
+// ------------------------------------------------------------------ host side
+
+inline int mg_init(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d) {
+  h.ndim = g.ndim;
+  h.S = g.S;
+  int n[3] = {g.nx, g.ny, g.nz};
+  const int minc = d.mg_min_coarse > 2 ? d.mg_min_coarse : 4;
+  if (d.mg_pre < 1 || d.mg_coarse_sweeps < 1 || d.mg_post < 0 || d.mg_max_cycles < 1) return CISDC_E_INVALID_ARGUMENT;
+  h.L = 0;
+  for (;;) {
+    MgLevel& L = h.lv[h.L];
+    L.nx = n[0];
+    L.ny = n[1];
+    L.nz = n[2];
+    L.ncell = (long long)n[0] * n[1] * n[2];
+    const size_t bytes = sizeof(double) * (size_t)L.ncell * g.S;
+    for (double** p : {&L.x, &L.t, &L.b}) {
+      void* v = nullptr;
+      if (cudaMalloc(&v, bytes) != cudaSuccess) return CISDC_E_CUDA;
+      h.allocs.push_back(v);
+      *p = static_cast<double*>(v);
+    }
+    h.L++;
+    bool ok = h.L < kMgMaxLevels;
+    for (int a = 0; a < g.ndim; ++a)
+      if (n[a] % 2 != 0 || n[a] / 2 < minc) ok = false;
+    if (!ok) break;
+    for (int a = 0; a < g.ndim; ++a) n[a] /= 2;
+  }
+  void* v = nullptr;
+  auto al = [&](size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    h.allocs.push_back(p);
+    return p;
+  };
+  h.d_active = static_cast<int*>(al(sizeof(int) * g.S));
+  h.d_cycles = static_cast<int*>(al(sizeof(int) * g.S));
+  h.d_bmax = static_cast<double*>(al(sizeof(double) * g.S));
+  h.d_rmax = static_cast<double*>(al(sizeof(double) * g.S));
+  h.d_flag = static_cast<int*>(al(sizeof(int) * 2));
+  if (!h.d_active || !h.d_cycles || !h.d_bmax || !h.d_rmax || !h.d_flag) return CISDC_E_CUDA;
+  if (cudaMallocHost(&v, sizeof(int) * 2) != cudaSuccess) return CISDC_E_CUDA;
+  h.h_flag = static_cast<int*>(v);
+  return CISDC_OK;
+}
+
+inline void mg_free(MgHierarchy& h) {
+  for (void* p : h.allocs) cudaFree(p);
+  h.allocs.clear();
+  if (h.h_flag) cudaFreeHost(h.h_flag);
+  h.h_flag = nullptr;
+}
+
+inline MgCoef mg_coef(const cisdc_problem_desc& d, int l, double coef) {
+  MgCoef C{};
+  C.ndim = d.ndim;
+  C.coef = coef;
+  for (int s = 0; s < d.nspecies; ++s) {
+    double csum = 0.0;
+    for (int a = 0; a < d.ndim; ++a) {
+      const double hl = d.h[a] * (double)(1 << l);
+      C.c[s][a] = d.diffusivity[s] / (12.0 * hl * hl);
+      csum = csum + C.c[s][a];
+    }
+    C.wD[s] = d.mg_omega / (1.0 + coef * (30.0 * csum));
+  }
+  return C;
+}
+
+template <int DIM>
+struct MgRunner {
+  MgHierarchy& h;
+  const cisdc_problem_desc& d;
+  MgCoef C[kMgMaxLevels];
+  cudaStream_t s;
+  long long* launches;
+  // level-0 x lives in h.lv[0].x (ping-pong with .t); b0 = rhs
+  const double* b0;
+
+  const double* bof(int l) const { return l == 0 ? b0 : h.lv[l].b; }
+  dim3 grid(long long ncell) const { return dim3((unsigned)((ncell + 255) / 256), (unsigned)h.S, 1); }
+
+  void smooth(int l, bool from_zero) {
+    MgLevel& L = h.lv[l];
+    k_mg_smooth<DIM><<<grid(L.ncell), 256, 0, s>>>(C[l], L.x, bof(l), L.t, L.nx, L.ny, L.nz, from_zero ? 1 : 0,
+                                                   h.d_active);
+    ++*launches;
+    std::swap(L.x, L.t);
+  }
+  void vcycle(int l) {
+    MgLevel& L = h.lv[l];
+    if (l == h.L - 1) {
+      for (int it = 0; it < d.mg_coarse_sweeps; ++it) smooth(l, l > 0 && it == 0);
+      return;
+    }
+    for (int it = 0; it < d.mg_pre; ++it) smooth(l, l > 0 && it == 0);
+    MgLevel& Cl = h.lv[l + 1];
+    k_mg_restrict<DIM><<<grid(Cl.ncell), 256, 0, s>>>(C[l], L.x, bof(l), L.nx, L.ny, L.nz, Cl.b, Cl.nx, Cl.ny, Cl.nz,
+                                                      h.d_active);
+    ++*launches;
+    vcycle(l + 1);
+    k_mg_prolong<DIM><<<grid(L.ncell), 256, 0, s>>>(L.x, L.nx, L.ny, L.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
+    ++*launches;
+    for (int it = 0; it < d.mg_post; ++it) smooth(l, false);
+  }
+};
+
+template <int DIM>
+inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
+                        double* out, DevStatus* st, cudaStream_t s, long long* launches) {
+  const long long n = g.n;
+  if (coef == 0.0) {
+    if (cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
+    return CISDC_OK;
+  }
+  MgRunner<DIM> R{h, d, {}, s, launches, rhs};
+  for (int l = 0; l < h.L; ++l) R.C[l] = mg_coef(d, l, coef);
+  std::vector<int> ones(g.S, 1);
+  cudaMemcpyAsync(h.d_active, ones.data(), sizeof(int) * g.S, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(h.d_cycles, 0, sizeof(int) * g.S, s);
+  cudaMemsetAsync(h.d_bmax, 0, sizeof(double) * g.S, s);
+  cudaMemsetAsync(h.d_rmax, 0, sizeof(double) * g.S, s);
+  cudaMemsetAsync(h.d_flag, 0, sizeof(int) * 2, s);
+  MgLevel& L0 = h.lv[0];
+  cudaMemcpyAsync(L0.x, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);  // x = b
+  const dim3 rgrid((unsigned)std::min<long long>((g.ncell + 255) / 256, 1184), (unsigned)g.S, 1);
+  k_mg_absmax<<<rgrid, 256, 0, s>>>(rhs, g.ncell, h.d_bmax);
+  *launches += 1;
+  for (;;) {
+    k_mg_resmax<DIM><<<rgrid, 256, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
+    k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax, h.d_flag,
+                                 st);
+    *launches += 2;
+    cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
+    if (!h.h_flag[0]) break;
+    R.vcycle(0);
+  }
+  if (cudaMemcpyAsync(out, L0.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
+  if (cudaGetLastError() != cudaSuccess) return CISDC_E_CUDA;
+  return CISDC_OK;
+}
+
+inline int mg_solve(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
+                    double* out, DevStatus* st, cudaStream_t s, long long* launches) {
+  switch (g.ndim) {
+    case 1: return mg_solve_dim<1>(h, g, d, coef, rhs, out, st, s, launches);
+    case 2: return mg_solve_dim<2>(h, g, d, coef, rhs, out, st, s, launches);
+    default: return mg_solve_dim<3>(h, g, d, coef, rhs, out, st, s, launches);
+  }
+}
+
+}  // namespace cisdc_b200

@@ -1,0 +1,149 @@
+// K2: spectral quadrature and sweep right-hand-side assembly, plus the increment norm (K5).
+//
+//  k_quad_base  -- quadrature_base (proj/core/src/integrators.cpp:52-65) for ALL M rows in one
+//                  pass: per element the M+1 node sums s_j = (fa+fd+fr)_j are formed once in
+//                  registers and contracted with the M x (M+1) matrix dt*Q (kernel parameter),
+//                  i.e. the S.F / Q.F product as a per-cell small-matrix contraction, not M passes.
+//  k_rhs        -- the stage right-hand sides of misdc_sweep (:86-87), misdcq_sweep (:115-122,
+//                  :127-134) and run_diffusion_cell (:201-226) in the reference's operand order.
+//  k_incr_*     -- increment_norm (proj/core/src/sweep_state.cpp:60-66): fixed-tree, run-to-run
+//                  deterministic sum (differs from the serial sum by rounding only).
+#pragma once
+
+#include "common.cuh"
+
+namespace cisdc_b200 {
+
+struct QuadArgs {
+  int M;
+  double c[kMaxM][kMaxM + 1];  // dt * Q(m, j)
+  const double* phi0;
+  const double* fa[kMaxM + 1];
+  const double* fd[kMaxM + 1];
+  const double* fr[kMaxM + 1];
+  double* base[kMaxM];
+};
+
+__global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadArgs q, long long n) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double s[kMaxM + 1];
+#pragma unroll
+  for (int j = 0; j <= kMaxM; ++j)
+    if (j <= q.M) s[j] = q.fa[j][e] + q.fd[j][e] + q.fr[j][e];
+  const double p0 = q.phi0[e];
+#pragma unroll
+  for (int m = 0; m < kMaxM; ++m) {
+    if (m >= q.M) break;
+    double acc = p0;
+#pragma unroll
+    for (int j = 0; j <= kMaxM; ++j)
+      if (j <= q.M) acc += q.c[m][j] * s[j];
+    q.base[m][e] = acc;
+  }
+}
+
+// One correction term: cE*(A - Ap) + cI*(D - Dp)                 (R == nullptr)
+//                   or cE*(A - Ap) + cI*(D - Dp + R - Rp)
+struct RhsTerm {
+  double cE, cI;
+  const double *A, *Ap, *D, *Dp, *R, *Rp;
+};
+
+enum RhsKind {
+  kRhsMisdcq = 0,  // out = base + sum(AD terms) - fc*X ; out2 = base + sum(ADR terms)
+  kRhsCisdcq = 1,  // out = base + sum(ADR terms) + (fc*(X - Y) - fc*Z)
+  kRhsMisdc = 2    // base = phi_m + sum_j sc_j*(fa+fd+fr)_j ; out = base + fc*(X - Y - Z)
+};
+
+struct RhsArgs {
+  int kind;
+  int nt;
+  RhsTerm t[kMaxM];
+  double fc;
+  const double *X, *Y, *Z;
+  const double* base;  // kRhsMisdcq / kRhsCisdcq
+  double* out;
+  double* out2;        // kRhsMisdcq: reaction-stage partial rhs (may be null)
+  // kRhsMisdc
+  int M;
+  double sc[kMaxM + 1];
+  const double* phim;
+  const double *sfa[kMaxM + 1], *sfd[kMaxM + 1], *sfr[kMaxM + 1];
+  double* base_out;
+};
+
+__global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, long long n) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  if (a.kind == kRhsMisdc) {
+    double base = a.phim[e];
+#pragma unroll
+    for (int j = 0; j <= kMaxM; ++j)
+      if (j <= a.M) base += a.sc[j] * (a.sfa[j][e] + a.sfd[j][e] + a.sfr[j][e]);
+    a.base_out[e] = base;
+    a.out[e] = base + a.fc * (a.X[e] - a.Y[e] - a.Z[e]);
+    return;
+  }
+  const double base = a.base[e];
+  if (a.kind == kRhsMisdcq) {
+    double rd = base, rr = base;
+#pragma unroll
+    for (int t = 0; t < kMaxM; ++t) {
+      if (t >= a.nt) break;
+      const RhsTerm& T = a.t[t];
+      const double dA = T.A[e] - T.Ap[e];
+      const double dD = T.D[e] - T.Dp[e];
+      rd += T.cE * dA + T.cI * dD;
+      if (a.out2) rr += T.cE * dA + T.cI * (dD + T.R[e] - T.Rp[e]);
+    }
+    rd -= a.fc * a.X[e];
+    a.out[e] = rd;
+    if (a.out2) a.out2[e] = rr;
+    return;
+  }
+  // kRhsCisdcq
+  double r = base;
+#pragma unroll
+  for (int t = 0; t < kMaxM; ++t) {
+    if (t >= a.nt) break;
+    const RhsTerm& T = a.t[t];
+    r += T.cE * (T.A[e] - T.Ap[e]) + T.cI * (T.D[e] - T.Dp[e] + T.R[e] - T.Rp[e]);
+  }
+  r += a.fc * (a.X[e] - a.Y[e]) - a.fc * a.Z[e];
+  a.out[e] = r;
+}
+
+constexpr int kIncrBlocks = 296;  // 2 x 148 SMs; fixed so the reduction tree is fixed
+constexpr int kIncrThreads = 256;
+
+__global__ void __launch_bounds__(kIncrThreads) k_incr_partial(const double* __restrict__ a,
+                                                              const double* __restrict__ b, long long n,
+                                                              double* __restrict__ partial) {
+  __shared__ double sh[kIncrThreads];
+  double s = 0.0;
+  for (long long e = (long long)blockIdx.x * kIncrThreads + threadIdx.x; e < n; e += (long long)kIncrBlocks * kIncrThreads)
+    s += fabs(a[e] - b[e]);
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = kIncrThreads / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
+}
+
+__global__ void k_incr_final(const double* __restrict__ a, const double* __restrict__ b, long long n,
+                             const double* __restrict__ partial, double* __restrict__ out) {
+  __shared__ double sh[512];
+  const int t = threadIdx.x;
+  sh[t] = t < kIncrBlocks ? partial[t] : 0.0;
+  __syncthreads();
+  for (int w = 256; w > 0; w >>= 1) {
+    if (t < w) sh[t] = sh[t] + sh[t + w];
+    __syncthreads();
+  }
+  if (t == 0) *out = (n == 1) ? fabs(a[0] - b[0]) : sh[0] / (double)n;
+}
+
+}  // namespace cisdc_b200

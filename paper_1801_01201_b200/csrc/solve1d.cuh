@@ -1,0 +1,265 @@
+// K3 (1-D): implicit diffusion solve (I - coef F_D) phi = rhs.
+//
+// Periodic 1-D (configs 1-2).  With the reference's 4th-order stencil the system is cyclic
+// pentadiagonal and, for constant coefficients, circulant:
+//     A = (1+30c) I - 16c (Z + Z^-1) + c (Z^2 + Z^-2),    c = coef * d / (12 h^2),
+// Z the cyclic shift.  It factors EXACTLY as A = K * P(Z) * P(Z^-1) with P(z) = 1 - p z + q z^2,
+// both roots of P outside the unit circle (host: cisdc_b200::factor_circulant).  The direct solve
+// is therefore two periodic second-order linear recurrences (a forward and a backward bidiagonal
+// pair) and a scale -- the "batched tri/bidiagonal" direct-solver family of the reference's
+// banded LU (proj/core/src/linalg.cpp:105-155), without its O(n) serial dependency chain.
+//
+// Each recurrence is evaluated as a parallel scan of 2x2 affine maps over ONE thread-block
+// cluster (up to 8 CTAs x 1024 threads x E elements): per-thread local recurrence -> CTA scan
+// (shared memory) -> cluster scan through distributed shared memory (DSMEM) -> periodic closure
+// s_{-1} = (I - T^N)^{-1} c_N -> per-thread re-run of the recurrence from its exact incoming
+// state.  The field is read once and written once; everything else stays on chip.
+//
+// Reference Dirichlet problem (config-0 gate): assemble_diffusion_system + banded_solve of
+// proj/core/src/problems/reaction_diffusion.cpp:127-164 executed verbatim by one thread
+// (bit-identical to the reference; the gate is n_x <= a few thousand).
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace cisdc_b200 {
+
+namespace cg = cooperative_groups;
+
+struct Circ {
+  int npass;
+  double p[4], q[4];
+  int reverse[4];
+  double invK;
+};
+
+struct Solve1dArgs {
+  const double* rhs;
+  double* out;
+  int N;
+  int active[kMaxS];  // 0: coef == 0 or d == 0 -> identity (copy)
+  Circ c[kMaxS];
+};
+
+struct Aff {  // s -> A s + c on the state (u_i, u_{i-1})
+  double a00, a01, a10, a11, c0, c1;
+};
+
+__device__ __forceinline__ Aff aff_identity() { return {1.0, 0.0, 0.0, 1.0, 0.0, 0.0}; }
+
+// later o earlier
+__device__ __forceinline__ Aff aff_then(const Aff& later, const Aff& earlier) {
+  Aff r;
+  r.a00 = later.a00 * earlier.a00 + later.a01 * earlier.a10;
+  r.a01 = later.a00 * earlier.a01 + later.a01 * earlier.a11;
+  r.a10 = later.a10 * earlier.a00 + later.a11 * earlier.a10;
+  r.a11 = later.a10 * earlier.a01 + later.a11 * earlier.a11;
+  r.c0 = later.a00 * earlier.c0 + later.a01 * earlier.c1 + later.c0;
+  r.c1 = later.a10 * earlier.c0 + later.a11 * earlier.c1 + later.c1;
+  return r;
+}
+
+template <int T>
+struct Solve1dSmem {
+  Aff scan[T];
+  Aff total[4];  // per pass: this CTA's total map (read by the cluster peers through DSMEM)
+};
+
+// One pass of the periodic recurrence u_i = (x_i + p u_{i-1}) - q u_{i-2} in visiting order.
+// pos: this thread's scan position; ranks in visiting order.
+template <int E, int T>
+__device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reverse, double p, double q,
+                                              Solve1dSmem<T>& sm, int pass, cg::cluster_group& cluster,
+                                              int cl_size) {
+  const int tid = threadIdx.x;
+  const int pos = reverse ? (T - 1 - tid) : tid;
+  const int my_rank = static_cast<int>(cluster.block_rank());
+  const int vrank = reverse ? (cl_size - 1 - my_rank) : my_rank;
+  // local map with zero incoming state
+  Aff m = aff_identity();
+  {
+    double s0 = 0.0, s1 = 0.0;
+    double a00 = 1.0, a01 = 0.0, a10 = 0.0, a11 = 1.0;
+#pragma unroll
+    for (int t = 0; t < E; ++t) {
+      if (t < len) {
+        const int e = reverse ? (len - 1 - t) : t;
+        const double un = (u[e] + p * s0) - q * s1;
+        s1 = s0;
+        s0 = un;
+        // A <- T A, T = [[p, -q], [1, 0]]
+        const double n00 = p * a00 - q * a10, n01 = p * a01 - q * a11;
+        a10 = a00;
+        a11 = a01;
+        a00 = n00;
+        a01 = n01;
+      }
+    }
+    m = {a00, a01, a10, a11, s0, s1};
+  }
+  // inclusive Hillis-Steele scan over positions within the CTA
+  sm.scan[pos] = m;
+  __syncthreads();
+  for (int off = 1; off < T; off <<= 1) {
+    Aff other = aff_identity();
+    const bool has = pos >= off;
+    if (has) other = sm.scan[pos - off];
+    __syncthreads();
+    if (has) {
+      m = aff_then(m, other);
+      sm.scan[pos] = m;
+    }
+    __syncthreads();
+  }
+  const Aff excl = pos > 0 ? sm.scan[pos - 1] : aff_identity();
+  if (pos == T - 1) sm.total[pass] = m;
+  cluster.sync();
+  // cluster prefix (CTAs before me in visiting order) and global total
+  Aff pre = aff_identity(), tot = aff_identity();
+  for (int v = 0; v < cl_size; ++v) {
+    const int r = reverse ? (cl_size - 1 - v) : v;
+    Solve1dSmem<T>* peer = cluster.map_shared_rank(&sm, r);
+    const Aff tv = peer->total[pass];
+    if (v < vrank) pre = aff_then(tv, pre);
+    tot = aff_then(tv, tot);
+  }
+  // periodic closure: s = (I - A_N)^{-1} c_N
+  const double m00 = 1.0 - tot.a00, m01 = -tot.a01, m10 = -tot.a10, m11 = 1.0 - tot.a11;
+  const double det = m00 * m11 - m01 * m10;
+  const double sa = (m11 * tot.c0 - m01 * tot.c1) / det;
+  const double sb = (m00 * tot.c1 - m10 * tot.c0) / det;
+  // incoming state of this CTA, then of this thread
+  const double ca = pre.a00 * sa + pre.a01 * sb + pre.c0;
+  const double cb = pre.a10 * sa + pre.a11 * sb + pre.c1;
+  double s0 = excl.a00 * ca + excl.a01 * cb + excl.c0;
+  double s1 = excl.a10 * ca + excl.a11 * cb + excl.c1;
+#pragma unroll
+  for (int t = 0; t < E; ++t) {
+    if (t < len) {
+      const int e = reverse ? (len - 1 - t) : t;
+      const double un = (u[e] + p * s0) - q * s1;
+      s1 = s0;
+      s0 = un;
+      u[e] = un;
+    }
+  }
+}
+
+// grid: (cluster_size * nsys) CTAs of T threads; cluster dims (cluster_size, 1, 1); one cluster per
+// species system (blockIdx.x / cluster_size).
+template <int E, int T>
+__global__ void __launch_bounds__(T) k_solve1d_periodic(const __grid_constant__ Solve1dArgs a) {
+  __shared__ Solve1dSmem<T> sm;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cl_size = static_cast<int>(cluster.num_blocks());
+  const int sys = blockIdx.x / cl_size;
+  const int rank = static_cast<int>(cluster.block_rank());
+  const int N = a.N;
+  const double* b = a.rhs + (long long)sys * N;
+  double* y = a.out + (long long)sys * N;
+  const int a0 = (rank * T + threadIdx.x) * E;
+  const int len = max(0, min(E, N - a0));
+  if (!a.active[sys]) {  // coef == 0: copy (reaction_diffusion.cpp:159)
+    for (int t = 0; t < len; ++t) y[a0 + t] = b[a0 + t];
+    return;  // uniform over the cluster: no cluster.sync below is reached by any CTA
+  }
+  const Circ& c = a.c[sys];
+  double u[E];
+#pragma unroll
+  for (int t = 0; t < E; ++t) u[t] = t < len ? b[a0 + t] : 0.0;
+  for (int k = 0; k < c.npass; ++k)
+    periodic_pass<E, T>(u, len, c.reverse[k] != 0, c.p[k], c.q[k], sm, k, cluster, cl_size);
+#pragma unroll
+  for (int t = 0; t < E; ++t)
+    if (t < len) y[a0 + t] = u[t] * c.invK;
+  cluster.sync();  // peers may still read this CTA's totals through DSMEM
+}
+
+// Reference Dirichlet system, one thread (bit-identical to assemble_diffusion_system + banded_solve)
+struct RdSolveArgs {
+  int n;
+  double c;  // coef * d / (12 dx^2), host-computed like the reference
+  double w[2][5];
+  const double* rhs;
+  double* out;
+  double* work;  // n * 10 doubles
+};
+
+__global__ void k_rd_banded_solve(RdSolveArgs a, DevStatus* st) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int n = a.n, kl = 3, ku = 3, width = 2 * kl + ku + 1;
+  const double kLap[5] = {-1.0, 16.0, -30.0, 16.0, -1.0};
+  double* w = a.work;
+  double* x = a.out;
+  for (long long i = 0; i < (long long)n * width; ++i) w[i] = 0.0;
+  // banded_solve copies A (band kl=ku=3) into a working band of width 2kl+ku+1 (row-major)
+#define W_(i, j) w[(long long)(i) * width + ((j) - (i) + kl)]
+  for (int i = 0; i < n; ++i) {
+    x[i] = a.rhs[i];
+    W_(i, i) = 1.0;
+  }
+  for (int i = 0; i < n; ++i) {
+    for (int o = -2; o <= 2; ++o) {
+      const double s = -a.c * kLap[o + 2];
+      const int j = i + o;
+      if (j >= 0 && j < n) {
+        W_(i, j) += s;
+      } else if (j < 0) {
+        const double* wg = a.w[-j - 1];
+        for (int q = 0; q < 4; ++q) W_(i, q) += s * wg[q + 1];
+        x[i] -= s * wg[0] * 1.0;
+      } else {
+        const double* wg = a.w[j - n];
+        for (int q = 0; q < 4; ++q) W_(i, n - 1 - q) += s * wg[q + 1];
+        x[i] -= s * wg[0] * 0.0;
+      }
+    }
+  }
+  for (int k = 0; k < n; ++k) {
+    const int last = min(n - 1, k + kl);
+    int p = k;
+    double best = fabs(W_(k, k));
+    for (int i = k + 1; i <= last; ++i) {
+      if (fabs(W_(i, k)) > best) {
+        best = fabs(W_(i, k));
+        p = i;
+      }
+    }
+    if (best == 0.0) {
+      atomicMin(&st->first_bad_cell, (unsigned long long)k);
+      atomicMax(&st->code, (int)CISDC_E_SOLVE);
+      st->stage = CISDC_STAGE_DIFFUSION;
+      return;
+    }
+    const int jmax = min(n - 1, k + kl + ku);
+    if (p != k) {
+      for (int j = k; j <= jmax; ++j) {
+        const double t = W_(k, j);
+        W_(k, j) = W_(p, j);
+        W_(p, j) = t;
+      }
+      const double t = x[k];
+      x[k] = x[p];
+      x[p] = t;
+    }
+    const double pivot = W_(k, k);
+    for (int i = k + 1; i <= last; ++i) {
+      const double m = W_(i, k) / pivot;
+      if (m != 0.0) {
+        for (int j = k + 1; j <= jmax; ++j) W_(i, j) -= m * W_(k, j);
+        x[i] -= m * x[k];
+      }
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = x[i];
+    const int jmax = min(n - 1, i + kl + ku);
+    for (int j = i + 1; j <= jmax; ++j) s -= W_(i, j) * x[j];
+    x[i] = s / W_(i, i);
+  }
+#undef W_
+}
+
+}  // namespace cisdc_b200
