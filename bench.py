@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 MISDC / PMISDC sweep engine (driver contract: one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config c5] [--scale 1]
+
+Workload (``config.workload``): BASELINE.json config 5 by default -- 3-D periodic 256^3 x 9 species
+mass-action ADR, 7 Gauss-Lobatto nodes (M = 6), 10 sweeps per step, PMISDC = CISDCQ nu = 1 with the
+D(m+1) || R(m) streams, multigrid to 1e-10 -- the largest configuration, on which BASELINE.md
+places the roofline claims (configs 1-2 are L2-resident / launch-bound; they are parity cases).
+A bench "step" is one SDC time step (initialise from phi^0, 10 sweeps): every step does identical
+work.  Metric: cell-species-node updates per second per sweep = n * M * sweeps / time.
+
+  value     device-resident inputs (cisdc_gpu_integrate_device), CUDA-event time on the engine's
+            stream, max over ranks; fields are >> L2 (1.2 GB each), no flush needed.
+  e2e       the reference-facing C-ABI call with HOST pinned buffers (cisdc_gpu_integrate): the
+            H2D of phi^0 and the D2H of the final state are inside every timed step.
+  roofline  dominant kernel class by live CUDA-event time; achieved = algorithmic bytes (HBM) or
+            analytic FP64 flops (Newton/LU) per launch / average launch time.
+  cpu_baseline  the UNMODIFIED reference (oracle/_ref, built from /root/reference) on a bounded
+            sample of the same workload (scaled grid), 1 core, rank 0 at N = 1.
+
+Multi-GPU: replicas only (no data-path collective); value = sum over ranks.
+--impl reference times the reference's CPU path (execute_pipelined with all useful host threads)
+on a bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# bounded CPU samples (grid scale divisor, steps) per config: ~10-30 s of reference CPU work
+CPU_SAMPLE = {"c0": (1, 20), "c1": (1, 100), "c2": (4, 4), "c3": (8, 1), "c4": (16, 1), "c5": (8, 1)}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--scale", type=int, default=1)
+    ap.add_argument("--scheme", type=int, default=None, help="override the config's scheme")
+    ap.add_argument("--workers", type=int, default=2, help="CISDCQ: >0 concurrent D/R streams")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_setup():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, v: float) -> float:
+    if ws <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows),
+                "power_w_max": max((float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()), default=None)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_reference_sample(cfg_name: str, scheme: int, workers: int, steps: int | None = None):
+    """Run the reference CPU path on the bounded sample; returns (updates/s, seconds, sample text, kind, cores)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle  # test infrastructure: the reference / its port, only as the CPU baseline
+    from paper_1801_01201_b200 import api, problems
+    scale, nsteps = CPU_SAMPLE.get(cfg_name, (8, 1))
+    if steps is not None:
+        nsteps = steps
+    spec = problems.CONFIGS[cfg_name](scale=scale) if cfg_name != "c0" else problems.config_c0()
+    opt = api.IntegrateOptions(scheme=scheme, dt=spec.dt, n_steps=nsteps, M=spec.M, n_sweeps=spec.n_sweeps,
+                               nu=spec.nu, workers=workers)
+    have_ref = oracle.ref_lib() is not None
+    t0 = time.perf_counter()
+    if have_ref:
+        oracle.ref_integrate(spec.problem, spec.phi0, opt)
+    else:
+        oracle.integrate(spec.problem, spec.phi0, opt)
+    dt = time.perf_counter() - t0
+    updates = spec.problem.dim * spec.M * spec.n_sweeps * nsteps
+    grid = "x".join(str(x) for x in spec.problem.n[: spec.problem.ndim])
+    sample = (f"{cfg_name} scaled 1/{scale} per axis: {grid} cells x {spec.problem.nspecies} species, "
+              f"{nsteps} step(s) x {spec.n_sweeps} sweeps, scheme {scheme}, workers {workers}")
+    return updates / dt, dt, sample, "reference" if have_ref else "port", max(1, workers if workers > 0 else 1)
+
+
+def run_reference_arm(args, ws, rank):
+    if rank != 0:
+        return
+    from paper_1801_01201_b200 import problems
+    spec = problems.CONFIGS[args.config](scale=CPU_SAMPLE.get(args.config, (8, 1))[0]) if args.config != "c0" \
+        else problems.config_c0()
+    scheme = spec.scheme if args.scheme is None else args.scheme
+    nproc = os.cpu_count() or 1
+    workers = min(nproc, max(2 * spec.nu, spec.M)) if scheme == 2 else 0
+    for _ in range(args.warmup):
+        cpu_reference_sample(args.config, scheme, workers, steps=1)
+    times, rates = [], []
+    sample = kind = None
+    cores = 1
+    for _ in range(args.steps):
+        r, t, sample, kind, cores = cpu_reference_sample(args.config, scheme, workers, steps=1)
+        times.append(t)
+        rates.append(r)
+    tot = float(np.sum(times))
+    value = float(np.mean(rates))
+    line = {
+        "impl": "reference", "metric": "cell-species-node updates/s per SDC sweep (FP64)", "value": value,
+        "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded BASELINE config generator)",
+        "config": {"workload": f"{args.config} (bounded CPU sample)", "scheme": scheme, "workers": workers},
+        "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, ws, rank)
+        return
+    import torch
+
+    from paper_1801_01201_b200 import _abi, api, problems, roofline
+    lib = _abi.load(build_if_missing=True)
+    torch.cuda.set_device(local)
+    spec = problems.CONFIGS[args.config](scale=args.scale) if args.config != "c0" else problems.config_c0()
+    scheme = spec.scheme if args.scheme is None else args.scheme
+    workers = args.workers if scheme == 2 else 0
+    desc = spec.problem
+    n = desc.dim
+    ctx = api.GpuContext(desc, spec.M, spec.convention)
+    opt = api.IntegrateOptions(scheme=scheme, dt=spec.dt, n_steps=1, M=spec.M, n_sweeps=spec.n_sweeps, nu=spec.nu,
+                               workers=workers, convention=spec.convention)
+    oc = opt.to_c()
+    rep = _abi.StepReportC()
+    incs = np.zeros(spec.n_sweeps)
+    d_phi0 = torch.from_numpy(spec.phi0).to(f"cuda:{local}")
+    d_out = torch.empty_like(d_phi0)
+    torch.cuda.synchronize()
+
+    def step_device():
+        ctx.check(lib.cisdc_gpu_integrate_device(ctx.h, C.c_void_p(d_phi0.data_ptr()), n, C.byref(oc),
+                                                 C.c_void_p(d_out.data_ptr()), C.byref(rep), _abi.dptr(incs)))
+        return rep.counters.newton_iterations
+
+    # FP64 peak (roofline denominator for the Newton/LU kernel; not in MEASURED_PEAKS.json)
+    pk_fma, pk_mul = C.c_double(), C.c_double()
+    lib.cisdc_gpu_fp64_peak(C.byref(pk_fma), C.byref(pk_mul))
+
+    for _ in range(args.warmup):
+        step_device()
+    lib.cisdc_gpu_kernel_times(ctx.h, None, None, None, 0, 1)  # reset
+    lib.cisdc_gpu_set_timing(ctx.h, 1)
+    newton = 0
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            newton += step_device()
+        torch.cuda.synchronize()
+    barrier(ws)
+    dev_ms = lib.cisdc_gpu_device_time_ms(ctx.h, 0)
+    ms = (C.c_double * 16)()
+    by = (C.c_double * 16)()
+    cnt = (C.c_longlong * 16)()
+    ncls = lib.cisdc_gpu_kernel_times(ctx.h, ms, by, cnt, 16, 1)
+    launches = int(lib.cisdc_gpu_launch_count(ctx.h))
+    lib.cisdc_gpu_set_timing(ctx.h, 0)
+    tmax = max_over_ranks(ws, dev_ms)
+    updates_per_step = n * spec.M * spec.n_sweeps
+    value = ws * updates_per_step * args.steps / (tmax * 1e-3)
+
+    # e2e: host pinned buffers through the C-ABI, copies inside every step
+    h_phi0 = torch.from_numpy(spec.phi0).pin_memory()
+    h_out = torch.empty_like(h_phi0).pin_memory()
+    for _ in range(1):
+        ctx.check(lib.cisdc_gpu_integrate(ctx.h, C.cast(h_phi0.data_ptr(), C.POINTER(C.c_double)), n, C.byref(oc),
+                                          C.cast(h_out.data_ptr(), C.POINTER(C.c_double)), C.byref(rep),
+                                          _abi.dptr(incs)))
+    lib.cisdc_gpu_device_time_ms(ctx.h, 1)
+    barrier(ws)
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.check(lib.cisdc_gpu_integrate(ctx.h, C.cast(h_phi0.data_ptr(), C.POINTER(C.c_double)), n, C.byref(oc),
+                                          C.cast(h_out.data_ptr(), C.POINTER(C.c_double)), C.byref(rep),
+                                          _abi.dptr(incs)))
+    wall = time.perf_counter() - wall0
+    e2e_ms = max_over_ranks(ws, lib.cisdc_gpu_device_time_ms(ctx.h, 1))
+    e2e_value = ws * updates_per_step * args.steps / (e2e_ms * 1e-3)
+
+    # roofline of the dominant kernel class
+    hbm, hbm_src = measured_peaks()
+    classes = []
+    for c in range(ncls):
+        if cnt[c] == 0:
+            continue
+        classes.append({"kernel": lib.cisdc_gpu_kernel_class_name(c).decode(), "ms": ms[c], "launches": int(cnt[c]),
+                        "share": ms[c] / max(sum(ms[:ncls]), 1e-30),
+                        "gbs": (by[c] / (ms[c] * 1e-3) / 1e9) if ms[c] > 0 else None})
+    dom = max(classes, key=lambda x: x["ms"])
+    cell_solves = desc.ncell * spec.M * spec.n_sweeps * args.steps * (spec.nu if scheme == 2 else 1)
+    newton_flops = roofline.newton_work(desc, newton, cell_solves)
+    if dom["kernel"] == "react_newton" and desc.nspecies >= 9:
+        achieved = newton_flops / (dom["ms"] * 1e-3) / 1e12
+        roof = {"bound": "fp64", "kernel": dom["kernel"], "achieved": achieved, "peak": pk_fma.value,
+                "unit": "TFLOP/s", "frac": achieved / pk_fma.value,
+                "peak_source": "measured DFMA chain peak on this GPU (cisdc_gpu_fp64_peak)",
+                "peak_dmul_dadd": pk_mul.value, "traffic": None,
+                "work": f"{newton} Newton trips, analytic {newton_flops:.3e} FP64 flops"}
+    else:
+        achieved = dom["gbs"]
+        roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": hbm_src, "traffic": None}
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            roof["traffic"] = json.load(f).get(roof["kernel"])
+
+    if rank == 0:
+        line = {
+            "metric": "cell-species-node updates/s per SDC sweep (FP64)",
+            "value": value, "unit": "updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded BASELINE config generator, problems.py)",
+            "config": {"workload": f"{args.config}: {spec.problem.name} {'x'.join(map(str, desc.n[:desc.ndim]))} "
+                                   f"x {desc.nspecies} species", "scheme": ["misdc", "misdcq", "cisdcq"][scheme],
+                       "nu": spec.nu, "workers": workers, "M": spec.M, "sweeps_per_step": spec.n_sweeps,
+                       "dt": spec.dt, "dofs": n, "updates_per_step": updates_per_step,
+                       "l2": "inputs larger than L2 (each field %.2f GB)" % (8 * n / 1e9),
+                       "parallelism": f"replicas x{ws}"},
+            "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
+                    "ms_per_step": e2e_ms / args.steps, "wall_s": wall},
+            "gpu_launches": launches,
+            "roofline": roof,
+            "kernels": sorted(classes, key=lambda x: -x["ms"]),
+            "end_to_end_hbm": {"algorithmic_bytes_per_sweep": 8.0 * n * (7 * spec.M + 4),
+                               "achieved_gbs": 8.0 * n * (7 * spec.M + 4) * spec.n_sweeps * args.steps / (tmax * 1e-3) / 1e9},
+            "newton_trips_per_cell_solve": newton / max(cell_solves, 1),
+        }
+        clk_s = clk.summary()
+        line["clocks"] = clk_s
+        if ws == 1 and not args.no_cpu_baseline:
+            v, t, sample, kind, cores = cpu_reference_sample(args.config, scheme, 0)
+            line["cpu_baseline"] = {"value": v, "unit": "updates/s", "cores": cores, "kind": kind, "sample": sample,
+                                    "seconds": t}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

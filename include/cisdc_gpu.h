@@ -65,7 +65,9 @@ enum {
   CISDC_REACTION_BISTABLE = 2,      /* R = lambda * phi (1 - phi) (phi - theta) (S = 1) */
   CISDC_REACTION_MASS_ACTION = 3    /* network of <=2-reactant/<=2-product mass-action reactions */
 };
-enum { CISDC_DIFFUSION_DIRECT = 0, CISDC_DIFFUSION_MULTIGRID = 1 };
+/* DIRECT: 1-D periodic exact circulant factorisation (blocked scan); MULTIGRID: 2-D/3-D;
+   BANDED_ORACLE: cyclic banded LU (reference banded_solve semantics), CPU oracle only (cross-check) */
+enum { CISDC_DIFFUSION_DIRECT = 0, CISDC_DIFFUSION_MULTIGRID = 1, CISDC_DIFFUSION_BANDED_ORACLE = 2 };
 enum { CISDC_FIELD_PHI = 0, CISDC_FIELD_FA = 1, CISDC_FIELD_FD = 2, CISDC_FIELD_FR = 3, CISDC_FIELD_PHI_AD = 4 };
 enum { CISDC_STAGE_ADVECTION = 0, CISDC_STAGE_DIFFUSION = 1, CISDC_STAGE_REACTION = 2 };
 
@@ -184,10 +186,19 @@ int cisdc_gpu_integrate_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t 
                                const cisdc_integrate_options* opt, double* d_final_state,
                                cisdc_step_report* reports, double* increments);
 
-/* device time (ms) of the kernels of the last sweep, by kernel class; returns count written */
-int cisdc_gpu_kernel_times(cisdc_gpu_ctx* ctx, double* ms /* [8] */, int enable);
-/* number of kernel launches issued by the last sweep */
+/* ---- measurement (no reference counterpart; used by bench.py) ----
+ * Live per-kernel-class CUDA-event timing on the launching stream (off by default), the
+ * algorithmic (compulsory) bytes each class moved and its launch count, accumulated since the
+ * last reset; the device time of sweep/integrate calls (events on the context's stream). */
+int cisdc_gpu_set_timing(cisdc_gpu_ctx* ctx, int on);
+int cisdc_gpu_kernel_times(cisdc_gpu_ctx* ctx, double* ms, double* bytes, long long* launches, int max_classes,
+                           int reset);
+const char* cisdc_gpu_kernel_class_name(int cls);
+double cisdc_gpu_device_time_ms(cisdc_gpu_ctx* ctx, int reset);
+/* kernel launches issued since creation (or the last kernel_times reset) */
 long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx);
+/* FP64 pipe peak on the current device: DFMA chains and DMUL+DADD chains, TFLOP/s */
+int cisdc_gpu_fp64_peak(double* tflops_dfma, double* tflops_dmul_dadd);
 
 #ifdef __cplusplus
 }

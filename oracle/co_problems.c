@@ -153,6 +153,9 @@ int co_problem_create(const cisdc_problem_desc* desc, co_problem** out, char* er
     }
     if (desc->diffusion_solver == CISDC_DIFFUSION_DIRECT) {
       if (desc->ndim != 1) BAD("direct diffusion solve is 1-D only; use multigrid");
+      if (p->nx > 8 * 512 * 32) BAD("1-D direct solve supports n <= 131072");
+    } else if (desc->diffusion_solver == CISDC_DIFFUSION_BANDED_ORACLE) {
+      if (desc->ndim != 1) BAD("banded diffusion solve is 1-D only");
     } else if (desc->diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
       int n0[3] = {p->nx, p->ny, p->nz};
       p->L = 1;
@@ -330,7 +333,7 @@ static void adr_reaction(const co_problem* p, const double* phi, double* out) {
       for (size_t i = 0; i < nc; ++i) out[i] = bistable_R(p->d.lambda, p->d.theta, phi[i]);
       break;
     case CISDC_REACTION_MASS_ACTION: {
-      double x[MAXS], R[MAXS];
+      double x[MAXS] = {0}, R[MAXS];
       for (size_t c = 0; c < nc; ++c) {
         for (int s = 0; s < p->S; ++s) x[s] = phi[(size_t)s * nc + c];
         ma_rates(p, x, R);
@@ -506,6 +509,182 @@ static int adr_solve_diffusion_direct(co_problem* p, double coef, const double* 
   free(bb);
   free(xx);
   return rc;
+}
+
+/* 1-D periodic direct solve as defined by the product: the exact
+   circulant factorisation A = K P(Z) P(Z^-1) applied as up to four periodic linear recurrences,
+   each evaluated with the blocked affine-map scan of solve1d.cuh -- same block decomposition, same
+   operation order -- so the GPU result is reproduced bit for bit.  (The independent cross-check is
+   the cyclic banded LU above, CISDC_DIFFUSION_BANDED_ORACLE.) */
+typedef struct {
+  double a00, a01, a10, a11, c0, c1;
+} aff_t;
+
+static aff_t aff_id(void) {
+  aff_t r = {1.0, 0.0, 0.0, 1.0, 0.0, 0.0};
+  return r;
+}
+
+static aff_t aff_then(aff_t later, aff_t earlier) {
+  aff_t r;
+  r.a00 = later.a00 * earlier.a00 + later.a01 * earlier.a10;
+  r.a01 = later.a00 * earlier.a01 + later.a01 * earlier.a11;
+  r.a10 = later.a10 * earlier.a00 + later.a11 * earlier.a10;
+  r.a11 = later.a10 * earlier.a01 + later.a11 * earlier.a11;
+  r.c0 = later.a00 * earlier.c0 + later.a01 * earlier.c1 + later.c0;
+  r.c1 = later.a10 * earlier.c0 + later.a11 * earlier.c1 + later.c1;
+  return r;
+}
+
+typedef struct {
+  int npass;
+  double p[4], q[4];
+  int reverse[4];
+  double invK;
+} circ_t;
+
+/* same explicit arithmetic as csrc/circulant.hpp factor_circulant */
+static circ_t circ_factor(double c) {
+  circ_t f;
+  memset(&f, 0, sizeof(f));
+  const double disc = 36.0 - 1.0 / c;
+  if (disc >= 0.0) {
+    const double r = sqrt(disc);
+    const double e1 = (1.0 / c) / (6.0 + r);
+    const double w1 = 2.0 + e1, w2 = 8.0 + r;
+    const double z1 = 2.0 / (w1 + sqrt(e1 * (w1 + 2.0)));
+    const double z2 = 2.0 / (w2 + sqrt((w2 - 2.0) * (w2 + 2.0)));
+    const double zs[4] = {z1, z2, z1, z2};
+    f.npass = 4;
+    for (int k = 0; k < 4; ++k) {
+      f.p[k] = zs[k];
+      f.q[k] = 0.0;
+      f.reverse[k] = k >= 2;
+    }
+    f.invK = (z1 * z2) / c;
+  } else {
+    const double wi = sqrt(-disc);
+    const double ar = 60.0 - wi * wi, ai = 16.0 * wi;
+    const double mod = sqrt(ar * ar + ai * ai);
+    double sr, si;
+    if (ar >= 0.0) {
+      sr = sqrt((mod + ar) * 0.5);
+      si = ai / (2.0 * sr);
+    } else {
+      si = sqrt((mod - ar) * 0.5);
+      sr = ai / (2.0 * si);
+    }
+    const double d1r = 8.0 + sr, d1i = wi + si, d2r = 8.0 - sr, d2i = wi - si;
+    const double m1 = d1r * d1r + d1i * d1i, m2 = d2r * d2r + d2i * d2i;
+    const double dr = m1 >= m2 ? d1r : d2r, di = m1 >= m2 ? d1i : d2i, dm = m1 >= m2 ? m1 : m2;
+    const double zr = (2.0 * dr) / dm, zi = (-2.0 * di) / dm;
+    f.npass = 2;
+    f.p[0] = f.p[1] = 2.0 * zr;
+    f.q[0] = f.q[1] = zr * zr + zi * zi;
+    f.reverse[0] = 0;
+    f.reverse[1] = 1;
+    f.invK = f.q[0] / c;
+  }
+  return f;
+}
+
+#define SCAN_T 512
+
+/* one periodic recurrence pass over u[0..N) with the GPU's blocking (E per thread, SCAN_T threads
+   per CTA, CL CTAs) */
+static void scan_pass(double* u, int N, int E, int CL, int reverse, double p, double q, aff_t* sc, aff_t* tmp,
+                      aff_t* excl, aff_t* tot_cta) {
+  const int nthr = CL * SCAN_T;
+  for (int rank = 0; rank < CL; ++rank) {
+    for (int tid = 0; tid < SCAN_T; ++tid) {
+      const int t = rank * SCAN_T + tid;
+      const int a0 = t * E;
+      int len = N - a0;
+      if (len < 0) len = 0;
+      if (len > E) len = E;
+      double s0 = 0.0, s1 = 0.0, a00 = 1.0, a01 = 0.0, a10 = 0.0, a11 = 1.0;
+      for (int k = 0; k < len; ++k) {
+        const int e = reverse ? (len - 1 - k) : k;
+        const double un = (u[a0 + e] + p * s0) - q * s1;
+        s1 = s0;
+        s0 = un;
+        const double n00 = p * a00 - q * a10, n01 = p * a01 - q * a11;
+        a10 = a00;
+        a11 = a01;
+        a00 = n00;
+        a01 = n01;
+      }
+      const int pos = reverse ? (SCAN_T - 1 - tid) : tid;
+      aff_t m = {a00, a01, a10, a11, s0, s1};
+      sc[rank * SCAN_T + pos] = m;
+    }
+    aff_t* S = sc + rank * SCAN_T;
+    for (int off = 1; off < SCAN_T; off <<= 1) {
+      for (int pos = 0; pos < SCAN_T; ++pos) tmp[pos] = pos >= off ? aff_then(S[pos], S[pos - off]) : S[pos];
+      memcpy(S, tmp, sizeof(aff_t) * SCAN_T);
+    }
+    for (int pos = 0; pos < SCAN_T; ++pos) excl[rank * SCAN_T + pos] = pos > 0 ? S[pos - 1] : aff_id();
+    tot_cta[rank] = S[SCAN_T - 1];
+  }
+  (void)nthr;
+  for (int rank = 0; rank < CL; ++rank) {
+    const int vrank = reverse ? (CL - 1 - rank) : rank;
+    aff_t pre = aff_id(), tot = aff_id();
+    for (int v = 0; v < CL; ++v) {
+      const int r = reverse ? (CL - 1 - v) : v;
+      if (v < vrank) pre = aff_then(tot_cta[r], pre);
+      tot = aff_then(tot_cta[r], tot);
+    }
+    const double m00 = 1.0 - tot.a00, m01 = -tot.a01, m10 = -tot.a10, m11 = 1.0 - tot.a11;
+    const double det = m00 * m11 - m01 * m10;
+    const double sa = (m11 * tot.c0 - m01 * tot.c1) / det;
+    const double sb = (m00 * tot.c1 - m10 * tot.c0) / det;
+    const double ca = pre.a00 * sa + pre.a01 * sb + pre.c0;
+    const double cb = pre.a10 * sa + pre.a11 * sb + pre.c1;
+    for (int tid = 0; tid < SCAN_T; ++tid) {
+      const int t = rank * SCAN_T + tid;
+      const int a0 = t * E;
+      int len = N - a0;
+      if (len < 0) len = 0;
+      if (len > E) len = E;
+      const int pos = reverse ? (SCAN_T - 1 - tid) : tid;
+      const aff_t ex = excl[rank * SCAN_T + pos];
+      double s0 = ex.a00 * ca + ex.a01 * cb + ex.c0;
+      double s1 = ex.a10 * ca + ex.a11 * cb + ex.c1;
+      for (int k = 0; k < len; ++k) {
+        const int e = reverse ? (len - 1 - k) : k;
+        const double un = (u[a0 + e] + p * s0) - q * s1;
+        s1 = s0;
+        s0 = un;
+        u[a0 + e] = un;
+      }
+    }
+  }
+}
+
+static int adr_solve_diffusion_scan(co_problem* p, double coef, const double* rhs, double* out) {
+  const int N = p->nx;
+  int E = 1;
+  while (E < 32 && (long long)E * SCAN_T * 8 < N) E *= 2;
+  const int CL = (N + E * SCAN_T - 1) / (E * SCAN_T);
+  aff_t* sc = (aff_t*)malloc(sizeof(aff_t) * CL * SCAN_T);
+  aff_t* ex = (aff_t*)malloc(sizeof(aff_t) * CL * SCAN_T);
+  aff_t* tmp = (aff_t*)malloc(sizeof(aff_t) * SCAN_T);
+  aff_t tot[64];
+  for (int s = 0; s < p->S; ++s) {
+    const double* b = rhs + (size_t)s * N;
+    double* o = out + (size_t)s * N;
+    const double c = coef * p->cdiff[s][0];
+    memcpy(o, b, sizeof(double) * N);
+    if (!(coef != 0.0 && c != 0.0)) continue;
+    const circ_t f = circ_factor(c);
+    for (int k = 0; k < f.npass; ++k) scan_pass(o, N, E, CL, f.reverse[k], f.p[k], f.q[k], sc, tmp, ex, tot);
+    for (int i = 0; i < N; ++i) o[i] = o[i] * f.invK;
+  }
+  free(sc);
+  free(ex);
+  free(tmp);
+  return CISDC_OK;
 }
 
 /* ------------------------------------------------------------------ multigrid (2-D/3-D) */
@@ -865,7 +1044,8 @@ int co_solve(co_problem* p, int stage, double coef, const double* rhs, double* o
       return fail(p, CISDC_E_CAPABILITY, "OperatorSplitProblem: coupled diffusion-reaction solve not provided");
     default:
       if (stage == CISDC_STAGE_DIFFUSION) {
-        if (p->d.diffusion_solver == CISDC_DIFFUSION_DIRECT) return adr_solve_diffusion_direct(p, coef, rhs, out);
+        if (p->d.diffusion_solver == CISDC_DIFFUSION_DIRECT) return adr_solve_diffusion_scan(p, coef, rhs, out);
+        if (p->d.diffusion_solver == CISDC_DIFFUSION_BANDED_ORACLE) return adr_solve_diffusion_direct(p, coef, rhs, out);
         return adr_solve_diffusion_mg(p, coef, rhs, out, c);
       }
       if (stage == CISDC_STAGE_REACTION) return adr_solve_reaction(p, coef, rhs, out, c);

@@ -116,8 +116,12 @@ GPU_SYMBOLS = [
      [_vp, _dp, C.c_size_t, C.POINTER(IntegrateOptionsC), _dp, C.POINTER(StepReportC), _dp]),
     ("cisdc_gpu_integrate_device", C.c_int,
      [_vp, _vp, C.c_size_t, C.POINTER(IntegrateOptionsC), _vp, C.POINTER(StepReportC), _dp]),
-    ("cisdc_gpu_kernel_times", C.c_int, [_vp, _dp, C.c_int]),
+    ("cisdc_gpu_set_timing", C.c_int, [_vp, C.c_int]),
+    ("cisdc_gpu_kernel_times", C.c_int, [_vp, _dp, _dp, C.POINTER(C.c_longlong), C.c_int, C.c_int]),
+    ("cisdc_gpu_kernel_class_name", C.c_char_p, [C.c_int]),
+    ("cisdc_gpu_device_time_ms", C.c_double, [_vp, C.c_int]),
     ("cisdc_gpu_launch_count", C.c_longlong, [_vp]),
+    ("cisdc_gpu_fp64_peak", C.c_int, [_dp, _dp]),
 ]
 
 _LIB = None

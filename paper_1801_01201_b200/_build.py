@@ -23,7 +23,7 @@ LIB = os.path.join(LIBDIR, "libcisdc_gpu.so")
 CU_SOURCES = ["cisdc_gpu.cu"]
 CXX_SOURCES = ["quadrature.cpp"]
 HEADERS = ["common.cuh", "stencil.cuh", "pointwise.cuh", "newton.cuh", "solve1d.cuh", "multigrid.cuh",
-           "circulant.hpp"]
+           "circulant.hpp", "peak.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

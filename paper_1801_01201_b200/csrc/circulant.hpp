@@ -3,10 +3,14 @@
 // With w = z + 1/z the symbol is c w^2 - 16 c w + (1 + 28 c), roots w = 8 -+ sqrt(36 - 1/c).
 // Each root gives zeta + 1/zeta = w with |zeta| < 1; p = zeta1 + zeta2, q = zeta1 zeta2 (real for
 // real roots and for a complex-conjugate pair), K = c / q.
+//
+// Written with explicit real arithmetic only (sqrt, +, -, *, /; no complex library calls) so the
+// CPU oracle (oracle/co_problems.c: circ_factor) reproduces the same bits.  The block
+// decomposition of the scan (solve1d_blocking) is part of the algorithm's definition for the same
+// reason: the oracle emulates the identical evaluation order.
 #pragma once
 
 #include <cmath>
-#include <complex>
 
 namespace cisdc_b200 {
 
@@ -20,13 +24,6 @@ struct CircFactor {
   int reverse[4];
   double invK;
 };
-
-inline std::complex<double> small_root(std::complex<double> w) {
-  // zeta = 2 / (w + sqrt(w^2 - 4)) with the sqrt branch that maximises |w + sqrt| (|zeta| < 1)
-  const std::complex<double> s = std::sqrt(w * w - 4.0);
-  const std::complex<double> d1 = w + s, d2 = w - s;
-  return 2.0 / (std::abs(d1) >= std::abs(d2) ? d1 : d2);
-}
 
 inline CircFactor factor_circulant(double c) {
   CircFactor f{};
@@ -47,15 +44,40 @@ inline CircFactor factor_circulant(double c) {
     }
     f.invK = (z1 * z2) / c;
   } else {
-    const std::complex<double> z = small_root(std::complex<double>(8.0, std::sqrt(-disc)));
+    // w = 8 + i wi; s = principal sqrt(w^2 - 4) = sqrt(ar + i ai)
+    const double wi = std::sqrt(-disc);
+    const double ar = 60.0 - wi * wi, ai = 16.0 * wi;
+    const double mod = std::sqrt(ar * ar + ai * ai);
+    double sr, si;
+    if (ar >= 0.0) {
+      sr = std::sqrt((mod + ar) * 0.5);
+      si = ai / (2.0 * sr);
+    } else {
+      si = std::sqrt((mod - ar) * 0.5);  // ai > 0
+      sr = ai / (2.0 * si);
+    }
+    // the denominator of larger modulus gives |zeta| < 1: zeta = 2 / (w +- s)
+    const double d1r = 8.0 + sr, d1i = wi + si, d2r = 8.0 - sr, d2i = wi - si;
+    const double m1 = d1r * d1r + d1i * d1i, m2 = d2r * d2r + d2i * d2i;
+    const double dr = m1 >= m2 ? d1r : d2r, di = m1 >= m2 ? d1i : d2i, dm = m1 >= m2 ? m1 : m2;
+    const double zr = (2.0 * dr) / dm, zi = (-2.0 * di) / dm;
     f.npass = 2;
-    f.p[0] = f.p[1] = 2.0 * z.real();
-    f.q[0] = f.q[1] = std::norm(z);
+    f.p[0] = f.p[1] = 2.0 * zr;
+    f.q[0] = f.q[1] = zr * zr + zi * zi;
     f.reverse[0] = 0;
     f.reverse[1] = 1;
     f.invK = f.q[0] / c;
   }
   return f;
+}
+
+// Block decomposition of the scan: T threads per CTA, E elements per thread, CL CTAs per cluster.
+constexpr int kSolve1dThreads = 512;
+inline void solve1d_blocking(int N, int* E, int* CL) {
+  int e = 1;
+  while (e < 32 && (long long)e * kSolve1dThreads * 8 < N) e *= 2;
+  *E = e;
+  *CL = (N + e * kSolve1dThreads - 1) / (e * kSolve1dThreads);
 }
 
 }  // namespace cisdc_b200

@@ -22,6 +22,7 @@
 #include "common.cuh"
 #include "multigrid.cuh"
 #include "newton.cuh"
+#include "peak.cuh"
 #include "pointwise.cuh"
 #include "solve1d.cuh"
 #include "stencil.cuh"
@@ -36,9 +37,67 @@ namespace {
 
 constexpr int kPhi = 0, kFa = 1, kFd = 2, kFr = 3;
 
-struct Status {
-  int code = CISDC_OK;
-  std::string msg;
+const char* kClassNames[kNumKernelClasses] = {"quad_base", "rhs", "solve1d", "mg_smooth", "mg_restrict",
+                                              "mg_prolong", "mg_norm", "react_newton", "eval_ad", "eval_r",
+                                              "increment"};
+
+// Launch accounting + optional live CUDA-event timing per kernel class.
+struct Timing final : LaunchHook {
+  bool on = false;
+  long long launches = 0;
+  double ms[kNumKernelClasses] = {};
+  double bytes[kNumKernelClasses] = {};
+  long long count[kNumKernelClasses] = {};
+  struct Pending {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<Pending> pending;
+  cudaEvent_t cur = nullptr;
+
+  cudaEvent_t take() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void before(int, cudaStream_t s) override {
+    if (!on) return;
+    cur = take();
+    cudaEventRecord(cur, s);
+  }
+  void after(int cls, cudaStream_t s, double b) override {
+    ++launches;
+    ++count[cls];
+    bytes[cls] += b;
+    if (!on) return;
+    cudaEvent_t e = take();
+    cudaEventRecord(e, s);
+    pending.push_back({cls, cur, e});
+  }
+  // call after the streams are synchronised
+  void resolve() {
+    for (const Pending& p : pending) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, p.a, p.b) == cudaSuccess) ms[p.cls] += t;
+    }
+    pending.clear();
+    used = 0;
+  }
+  void reset() {
+    for (int c = 0; c < kNumKernelClasses; ++c) {
+      ms[c] = bytes[c] = 0.0;
+      count[c] = 0;
+    }
+    launches = 0;
+  }
+  ~Timing() override {
+    for (cudaEvent_t e : pool) cudaEventDestroy(e);
+  }
 };
 
 }  // namespace
@@ -67,7 +126,6 @@ struct cisdc_gpu_ctx {
   double* fa_ad[kMaxM + 1] = {};
   double* fd_ad[kMaxM + 1] = {};
   std::vector<double*> slot_bufs;  // (nu-1) * M * 5: phi_ad, phi_r, fa_r, fd_r, fr_r
-  int slot_nu = 1;
   // solvers
   double* rd_work = nullptr;
   MgHierarchy mg;
@@ -75,19 +133,23 @@ struct cisdc_gpu_ctx {
   DevStatus* d_st = nullptr;
   DevStatus* h_st = nullptr;  // pinned
   double* d_partial = nullptr;
-  double* d_incr = nullptr;
-  double* h_incr = nullptr;   // pinned
+  double* d_incr = nullptr;   // [kMaxSweepsPerStep] increments of the current step
+  double* h_incr = nullptr;   // pinned mirror
+  int incr_slot = 0;
   unsigned long long newton_seen = 0, mg_seen = 0;
   cudaStream_t s_main = nullptr, s_r = nullptr;
   std::vector<cudaEvent_t> ev_pool;
-  cudaEvent_t ev_base = nullptr, ev_join = nullptr;
-  long long launches = 0;
+  cudaEvent_t ev_base = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  Timing tm;
+  double device_ms = 0.0;
   std::string err;
   double last_incr = 0.0;
   bool have_incr = false;
 };
 
 namespace {
+
+constexpr int kMaxSweepsPerStep = 4096;
 
 int set_err(cisdc_gpu_ctx* c, int code, const std::string& m) {
   if (c) c->err = m;
@@ -100,6 +162,12 @@ int set_err(cisdc_gpu_ctx* c, int code, const std::string& m) {
     if (e_ != cudaSuccess)                                                                       \
       return set_err(ctx, CISDC_E_CUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
                                             " at " #x);                                          \
+  } while (0)
+
+#define TRY(x)             \
+  do {                     \
+    const int rc_ = (x);   \
+    if (rc_) return rc_;   \
   } while (0)
 
 int dalloc(cisdc_gpu_ctx* ctx, double** p, size_t count) {
@@ -126,24 +194,28 @@ void alias_views_to_node0(cisdc_gpu_ctx* c, int set) {
 
 int grid_of(long long n, int block) { return static_cast<int>((n + block - 1) / block); }
 
+double F8(const cisdc_gpu_ctx* c) { return 8.0 * (double)c->g.n; }  // bytes of one field
+
 // ---------------------------------------------------------------- kernel launchers
 
 int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd, cudaStream_t s) {
   const int blocks = grid_of(ctx->g.n, 256);
+  ctx->tm.before(kKEvalAD, s);
   switch (ctx->g.ndim) {
     case 1: k_eval_ad<1><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
     case 2: k_eval_ad<2><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
     default: k_eval_ad<3><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
   }
-  ++ctx->launches;
+  ctx->tm.after(kKEvalAD, s, F8(ctx) * (1 + (fa != nullptr) + (fd != nullptr)));
   CU(cudaGetLastError());
   return CISDC_OK;
 }
 
 template <int S>
 int launch_eval_r_s(cisdc_gpu_ctx* ctx, const double* phi, double* fr, cudaStream_t s) {
+  ctx->tm.before(kKEvalR, s);
   k_eval_r<S><<<grid_of(ctx->g.ncell, 128), 128, 0, s>>>(ctx->rx, ctx->g, phi, fr);
-  ++ctx->launches;
+  ctx->tm.after(kKEvalR, s, 2.0 * F8(ctx));
   CU(cudaGetLastError());
   return CISDC_OK;
 }
@@ -159,9 +231,21 @@ int launch_eval_r(cisdc_gpu_ctx* ctx, const double* phi, double* fr, cudaStream_
   return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unsupported species count");
 }
 
+// compulsory fields touched by one reaction-stage launch
+double react_fields(int mode, const ReactArgs& a) {
+  const double w = 1.0 + (a.fr_out != nullptr);
+  switch (mode) {
+    case kModeMisdcq: return 4.0 + w;
+    case kModeMisdc: return 6.0 + w;
+    case kModeCisdcq: return (a.has_incr ? 4.0 : 2.0) + w;
+    default: return 1.0 + w;
+  }
+}
+
 template <int S, int MODE>
 int launch_react_sm(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   const int blocks = grid_of(ctx->g.ncell, 128);
+  ctx->tm.before(kKReact, s);
   if constexpr (MODE == kModeMisdcq || MODE == kModeMisdc) {
     switch (ctx->g.ndim) {
       case 1: k_react<S, 1, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
@@ -171,7 +255,7 @@ int launch_react_sm(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   } else {
     k_react<S, 1, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
   }
-  ++ctx->launches;
+  ctx->tm.after(kKReact, s, F8(ctx) * react_fields(MODE, a));
   CU(cudaGetLastError());
   return CISDC_OK;
 }
@@ -198,8 +282,13 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t 
 }
 
 int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
+  double fields;
+  if (a.kind == kRhsMisdc) fields = 1 + 3.0 * (a.M + 1) + 3 + 2;
+  else if (a.kind == kRhsMisdcq) fields = 1 + 6.0 * a.nt + 1 + 1 + (a.out2 != nullptr);
+  else fields = 1 + 6.0 * a.nt + 3 + 1;
+  ctx->tm.before(kKRhs, s);
   k_rhs<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(a, ctx->g.n);
-  ++ctx->launches;
+  ctx->tm.after(kKRhs, s, F8(ctx) * fields);
   CU(cudaGetLastError());
   return CISDC_OK;
 }
@@ -217,15 +306,16 @@ int launch_quad_base(cisdc_gpu_ctx* ctx, int set, double dt, cudaStream_t s) {
     q.fr[j] = V(ctx, set, kFr, j);
   }
   for (int m = 0; m < M; ++m) q.base[m] = ctx->base[m];
+  ctx->tm.before(kKQuad, s);
   k_quad_base<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(q, ctx->g.n);
-  ++ctx->launches;
+  ctx->tm.after(kKQuad, s, F8(ctx) * (1 + 3.0 * (M + 1) + M));
   CU(cudaGetLastError());
   return CISDC_OK;
 }
 
 template <int E>
 int launch_solve1d_e(cisdc_gpu_ctx* ctx, const Solve1dArgs& a, int cl, cudaStream_t s) {
-  constexpr int T = 512;
+  constexpr int T = kSolve1dThreads;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(cl * ctx->S, 1, 1);
   cfg.blockDim = dim3(T, 1, 1);
@@ -238,8 +328,9 @@ int launch_solve1d_e(cisdc_gpu_ctx* ctx, const Solve1dArgs& a, int cl, cudaStrea
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  ctx->tm.before(kKSolve1d, s);
   CU(cudaLaunchKernelEx(&cfg, k_solve1d_periodic<E, T>, a));
-  ++ctx->launches;
+  ctx->tm.after(kKSolve1d, s, 2.0 * F8(ctx));
   return CISDC_OK;
 }
 
@@ -258,13 +349,14 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
     a.rhs = rhs;
     a.out = out;
     a.work = ctx->rd_work;
+    ctx->tm.before(kKSolve1d, s);
     k_rd_banded_solve<<<1, 32, 0, s>>>(a, ctx->d_st);
-    ++ctx->launches;
+    ctx->tm.after(kKSolve1d, s, 2.0 * F8(ctx));
     CU(cudaGetLastError());
     return CISDC_OK;
   }
   if (ctx->desc.diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
-    const int rc = mg_solve(ctx->mg, ctx->g, ctx->desc, coef, rhs, out, ctx->d_st, s, &ctx->launches);
+    const int rc = mg_solve(ctx->mg, ctx->g, ctx->desc, coef, rhs, out, ctx->d_st, s, &ctx->tm);
     if (rc) return set_err(ctx, rc, "multigrid launch failed");
     return CISDC_OK;
   }
@@ -287,11 +379,8 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
       a.c[sp].invK = f.invK;
     }
   }
-  const int N = ctx->g.nx;
-  const int T = 512;
-  int E = 1;
-  while (E < 32 && (long long)E * T * 8 < N) E *= 2;
-  const int cl = (N + E * T - 1) / (E * T);
+  int E = 1, cl = 1;
+  solve1d_blocking(ctx->g.nx, &E, &cl);
   switch (E) {
     case 1: return launch_solve1d_e<1>(ctx, a, cl, s);
     case 2: return launch_solve1d_e<2>(ctx, a, cl, s);
@@ -302,19 +391,25 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
   }
 }
 
-int launch_incr(cisdc_gpu_ctx* ctx, const double* a, const double* b, cudaStream_t s) {
+int launch_incr(cisdc_gpu_ctx* ctx, const double* a, const double* b, double* out, cudaStream_t s) {
+  ctx->tm.before(kKIncr, s);
   k_incr_partial<<<kIncrBlocks, kIncrThreads, 0, s>>>(a, b, ctx->g.n, ctx->d_partial);
-  k_incr_final<<<1, 512, 0, s>>>(a, b, ctx->g.n, ctx->d_partial, ctx->d_incr);
-  ctx->launches += 2;
+  ctx->tm.after(kKIncr, s, 2.0 * F8(ctx));
+  ctx->tm.before(kKIncr, s);
+  k_incr_final<<<1, 512, 0, s>>>(a, b, ctx->g.n, ctx->d_partial, out);
+  ctx->tm.after(kKIncr, s, 0.0);
   CU(cudaGetLastError());
   return CISDC_OK;
 }
 
 // ---------------------------------------------------------------- status
 
-int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters, cudaStream_t s) {
+// Synchronises s_main, harvests timing and the device status word.
+int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters) {
+  cudaStream_t s = ctx->s_main;
   CU(cudaMemcpyAsync(ctx->h_st, ctx->d_st, sizeof(DevStatus), cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
+  ctx->tm.resolve();
   const DevStatus h = *ctx->h_st;
   if (counters) {
     counters->newton_iterations += (long long)(h.newton_trips - ctx->newton_seen);
@@ -334,8 +429,7 @@ int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters, cudaStream_t s) {
       std::snprintf(buf, sizeof(buf), "solve_diffusion: multigrid: species %llu: no convergence in %d cycles",
                     h.first_bad_cell, ctx->desc.mg_max_cycles);
     }
-    // reset the status word so the context stays usable
-    DevStatus z{};
+    DevStatus z{};  // reset the status word so the context stays usable
     z.first_bad_cell = ~0ull;
     z.newton_trips = h.newton_trips;
     z.mg_cycles = h.mg_cycles;
@@ -348,15 +442,10 @@ int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters, cudaStream_t s) {
 
 // ---------------------------------------------------------------- sweeps
 
-#define TRY(x)                  \
-  do {                          \
-    const int rc_ = (x);        \
-    if (rc_) return rc_;        \
-  } while (0)
-
 double QI(const cisdc_tables& t, int m, int j) { return t.QtI[m * t.M + j]; }
 double QE(const cisdc_tables& t, int m, int j) { return t.QtE[m * t.M + j]; }
 
+// misdcq_sweep (integrators.cpp:103-143)
 int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
   const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
   cudaStream_t s = ctx->s_main;
@@ -401,6 +490,7 @@ int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
   return CISDC_OK;
 }
 
+// misdc_sweep (integrators.cpp:69-101)
 int sweep_misdc(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
   const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
   cudaStream_t s = ctx->s_main;
@@ -471,6 +561,7 @@ int ensure_slots(cisdc_gpu_ctx* ctx, int nu) {
   return CISDC_OK;
 }
 
+// cisdcq_cells::run_diffusion_cell (integrators.cpp:195-235)
 int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c) {
   const int prev = ctx->cur, row = m - 1;
   RhsArgs r{};
@@ -514,6 +605,7 @@ int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt
   return CISDC_OK;
 }
 
+// cisdcq_cells::run_reaction_cell (integrators.cpp:237-258)
 int reaction_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c) {
   const int prev = ctx->cur, row = m - 1;
   ReactArgs a{};
@@ -534,6 +626,7 @@ int reaction_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt,
   return CISDC_OK;
 }
 
+// cisdcq_sweep (workers == 0, integrators.cpp:273-288) or execute_pipelined (pipeline.cpp:171-320)
 int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_counters* c) {
   if (nu < 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "cisdcq_sweep: nu must be >= 1");
   const int M = ctx->M, nxt = 1 - ctx->cur;
@@ -543,7 +636,6 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   cudaStream_t sd = ctx->s_main;
   TRY(launch_quad_base(ctx, ctx->cur, dt, sd));
   if (workers <= 0) {
-    // cisdcq_sweep order (integrators.cpp:281-286): for ell, for m: D then R
     for (int ell = 1; ell <= nu; ++ell)
       for (int m = 1; m <= M; ++m) {
         TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c));
@@ -551,8 +643,9 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
       }
     return CISDC_OK;
   }
-  // execute_pipelined (pipeline.cpp:36-70 edges): D cells on s_main, R cells on s_r; the
+  // DAG of build_task_graph (pipeline.cpp:36-70): D cells on s_main, R cells on s_r; the
   // cross-stream edges D(m,l) -> R(m,l) and R(m-2,l), R(m-1,l-1), R(m,l-1) -> D(m,l) are events.
+  // D cells are totally ordered on their stream (single rhs buffer); R cells write only their slots.
   cudaStream_t sr = ctx->s_r;
   const size_t ncells = (size_t)M * nu;
   while (ctx->ev_pool.size() < 2 * ncells) {
@@ -564,8 +657,6 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   auto evR = [&](int m, int ell) { return ctx->ev_pool[2 * ((size_t)(ell - 1) * M + (m - 1)) + 1]; };
   CU(cudaEventRecord(ctx->ev_base, sd));
   CU(cudaStreamWaitEvent(sr, ctx->ev_base, 0));
-  // the D stream needs a single rhs buffer (D cells are totally ordered on it); R cells write
-  // only their own slots.
   for (int ell = 1; ell <= nu; ++ell) {
     for (int m = 1; m <= M; ++m) {
       if (m >= 3) CU(cudaStreamWaitEvent(sd, evR(m - 2, ell), 0));
@@ -598,7 +689,8 @@ int do_initialize(cisdc_gpu_ctx* ctx) {
   return CISDC_OK;
 }
 
-int run_one_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers, cisdc_counters* c) {
+// one sweep, asynchronous; the increment lands in d_incr[slot]
+int run_one_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers, cisdc_counters* c, int slot) {
   const int prev = ctx->cur;
   const double* prev_end = V(ctx, prev, kPhi, ctx->M);
   switch (scheme) {
@@ -610,8 +702,22 @@ int run_one_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers
     default: return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown scheme");
   }
   const int nxt = 1 - prev;
-  TRY(launch_incr(ctx, V(ctx, nxt, kPhi, ctx->M), prev_end, ctx->s_main));
+  TRY(launch_incr(ctx, V(ctx, nxt, kPhi, ctx->M), prev_end, ctx->d_incr + slot, ctx->s_main));
   ctx->cur = nxt;
+  return CISDC_OK;
+}
+
+int begin_timed(cisdc_gpu_ctx* ctx) {
+  CU(cudaEventRecord(ctx->ev_t0, ctx->s_main));
+  return CISDC_OK;
+}
+
+int end_timed(cisdc_gpu_ctx* ctx) {
+  CU(cudaEventRecord(ctx->ev_t1, ctx->s_main));
+  CU(cudaEventSynchronize(ctx->ev_t1));
+  float t = 0.f;
+  CU(cudaEventElapsedTime(&t, ctx->ev_t0, ctx->ev_t1));
+  ctx->device_ms += t;
   return CISDC_OK;
 }
 
@@ -623,7 +729,7 @@ extern "C" {
 
 const char* cisdc_gpu_last_error(const cisdc_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 size_t cisdc_gpu_dimension(const cisdc_gpu_ctx* ctx) { return ctx ? (size_t)ctx->g.n : 0; }
-long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx) { return ctx ? ctx->tm.launches : 0; }
 
 void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
   if (!ctx) return;
@@ -633,8 +739,8 @@ void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   if (ctx->h_incr) cudaFreeHost(ctx->h_incr);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
-  if (ctx->ev_base) cudaEventDestroy(ctx->ev_base);
-  if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+  for (cudaEvent_t e : {ctx->ev_base, ctx->ev_join, ctx->ev_t0, ctx->ev_t1})
+    if (e) cudaEventDestroy(e);
   if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
   if (ctx->s_r) cudaStreamDestroy(ctx->s_r);
   delete ctx;
@@ -664,7 +770,7 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     static const double pts[5] = {0.0, 0.5, 1.5, 2.5, 3.5};
     const double xg[2] = {-0.5, -1.5};
     for (int k = 0; k < 2; ++k)
-      for (int j = 0; j < 5; ++j) {
+      for (int j = 0; j < 5; ++j) {  // lagrange_weights_at, reaction_diffusion.cpp:34-46
         double num = 1.0, den = 1.0;
         for (int i = 0; i < 5; ++i) {
           if (i == j) continue;
@@ -727,7 +833,8 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
           if (a >= 0) rx.nu[a][r] -= 1;
           if (p >= 0) rx.nu[p][r] += 1;
         }
-        if (rx.reac[r][0] < 0) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: every reaction needs a first reactant");
+        if (rx.reac[r][0] < 0)
+          return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: every reaction needs a first reactant");
         rx.k[r] = d->rate_constants[r];
       }
     } else if (d->reaction_kind != CISDC_REACTION_NONE) {
@@ -735,9 +842,9 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     }
     if (d->diffusion_solver == CISDC_DIFFUSION_DIRECT) {
       if (d->ndim != 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "direct diffusion solve is 1-D only; use multigrid");
-      if (g.nx > 8 * 512 * 32) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "1-D direct solve supports n <= 131072");
+      if (g.nx > 8 * kSolve1dThreads * 32) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "1-D direct solve supports n <= 131072");
     } else if (d->diffusion_solver != CISDC_DIFFUSION_MULTIGRID) {
-      return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown diffusion solver");
+      return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "diffusion solver not available on the GPU (oracle-only)");
     }
   } else if (d->kind == CISDC_PROBLEM_LINEAR_SCALAR) {
     return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "linear scalar problem is oracle-only (dimension 1)");
@@ -776,12 +883,14 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
   CU(cudaMemcpy(ctx->d_st, &z, sizeof(z), cudaMemcpyHostToDevice));
   CU(cudaMallocHost(&ctx->h_st, sizeof(DevStatus)));
   TRY(dalloc(ctx, &ctx->d_partial, kIncrBlocks));
-  TRY(dalloc(ctx, &ctx->d_incr, 1));
-  CU(cudaMallocHost(&ctx->h_incr, sizeof(double)));
+  TRY(dalloc(ctx, &ctx->d_incr, kMaxSweepsPerStep));
+  CU(cudaMallocHost(&ctx->h_incr, sizeof(double) * kMaxSweepsPerStep));
   CU(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&ctx->s_r, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&ctx->ev_base, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+  CU(cudaEventCreate(&ctx->ev_t0));
+  CU(cudaEventCreate(&ctx->ev_t1));
   reset_views(ctx, 0);
   reset_views(ctx, 1);
   return CISDC_OK;
@@ -793,9 +902,8 @@ int cisdc_gpu_create(const cisdc_problem_desc* desc, const cisdc_tables* tables,
   cisdc_gpu_ctx* ctx = new cisdc_gpu_ctx();
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-    // keep the context so the caller can read the message
     ctx->err = "no CUDA device: the B200 sweep engine has no CPU fallback";
-    *out = ctx;
+    *out = ctx;  // the caller reads the message, then destroys
     return CISDC_E_CUDA;
   }
   const int rc = build_ctx(ctx, desc, tables);
@@ -808,8 +916,7 @@ int cisdc_gpu_initialize(cisdc_gpu_ctx* ctx, const double* phi0, size_t n) {
   if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "SweepState::initialize: dimension mismatch");
   CU(cudaMemcpyAsync(ctx->node0[kPhi], phi0, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->s_main));
   TRY(do_initialize(ctx));
-  CU(cudaStreamSynchronize(ctx->s_main));
-  return CISDC_OK;
+  return check_status(ctx, nullptr);
 }
 
 int cisdc_gpu_initialize_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t n) {
@@ -817,8 +924,7 @@ int cisdc_gpu_initialize_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t
   if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "SweepState::initialize: dimension mismatch");
   CU(cudaMemcpyAsync(ctx->node0[kPhi], d_phi0, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->s_main));
   TRY(do_initialize(ctx));
-  CU(cudaStreamSynchronize(ctx->s_main));
-  return CISDC_OK;
+  return check_status(ctx, nullptr);
 }
 
 int cisdc_gpu_set_nodes(cisdc_gpu_ctx* ctx, const double* values, size_t n) {
@@ -838,17 +944,17 @@ int cisdc_gpu_set_nodes(cisdc_gpu_ctx* ctx, const double* values, size_t n) {
     TRY(launch_eval_r(ctx, phi, fr, s));
   }
   ctx->have_incr = false;
-  CU(cudaStreamSynchronize(s));
-  return CISDC_OK;
+  return check_status(ctx, nullptr);
 }
 
 int cisdc_gpu_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers, cisdc_counters* inout) {
   TRY(check_ctx(ctx));
-  ctx->launches = 0;
-  TRY(run_one_sweep(ctx, scheme, dt, nu, workers, inout));
+  TRY(begin_timed(ctx));
+  TRY(run_one_sweep(ctx, scheme, dt, nu, workers, inout, 0));
   CU(cudaMemcpyAsync(ctx->h_incr, ctx->d_incr, sizeof(double), cudaMemcpyDeviceToHost, ctx->s_main));
-  TRY(check_status(ctx, inout, ctx->s_main));
-  ctx->last_incr = *ctx->h_incr;
+  TRY(end_timed(ctx));
+  TRY(check_status(ctx, inout));
+  ctx->last_incr = ctx->h_incr[0];
   ctx->have_incr = true;
   return CISDC_OK;
 }
@@ -895,10 +1001,10 @@ int cisdc_gpu_eval(cisdc_gpu_ctx* ctx, int stage, const double* phi, double* out
   CU(cudaMemcpyAsync(ctx->rhs_d, phi, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   if (stage == CISDC_STAGE_ADVECTION) TRY(launch_eval_ad(ctx, ctx->rhs_d, ctx->scratch, nullptr, s));
   else if (stage == CISDC_STAGE_DIFFUSION) TRY(launch_eval_ad(ctx, ctx->rhs_d, nullptr, ctx->scratch, s));
-  else TRY(launch_eval_r(ctx, ctx->rhs_d, ctx->scratch, s));
+  else if (stage == CISDC_STAGE_REACTION) TRY(launch_eval_r(ctx, ctx->rhs_d, ctx->scratch, s));
+  else return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown stage");
   CU(cudaMemcpyAsync(out, ctx->scratch, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  return CISDC_OK;
+  return check_status(ctx, nullptr);
 }
 
 int cisdc_gpu_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rhs, double* out, size_t n,
@@ -919,65 +1025,77 @@ int cisdc_gpu_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rh
   } else {
     return set_err(ctx, CISDC_E_CAPABILITY, "OperatorSplitProblem: coupled diffusion-reaction solve not provided");
   }
-  TRY(check_status(ctx, inout, s));
+  TRY(check_status(ctx, inout));
   CU(cudaMemcpy(out, ctx->scratch, sizeof(double) * n, cudaMemcpyDeviceToHost));
   return CISDC_OK;
 }
 
+// cisdc::integrate (integrators.cpp:301-333).  Sweeps are enqueued asynchronously; without a
+// stop tolerance the host synchronises once per step (increments and counters are harvested
+// from device memory), with one it must look at every increment.
 static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_device, size_t n,
                           const cisdc_integrate_options* o, double* final_state, bool final_device,
                           cisdc_step_report* reports, double* increments) {
   TRY(check_ctx(ctx));
   if (!o) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: null options");
   if (o->n_sweeps < 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: n_sweeps must be >= 1");
+  if (o->n_sweeps > kMaxSweepsPerStep) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: too many sweeps");
   if (o->scheme == CISDC_SCHEME_CISDCQ && o->nu < 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: nu must be >= 1");
   if (o->M != ctx->M) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: options.M differs from the context's tables");
   if (n != (size_t)ctx->g.n) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "integrate: dimension mismatch");
-  // the context's tables must be make_quadrature_tables(M, convention)
-  if (o->convention != ctx->tb.convention) {
+  if (o->convention != ctx->tb.convention) {  // tables = make_quadrature_tables(M, convention)
     cisdc_tables t;
     if (make_tables(o->M, o->convention, &t)) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "bad tables");
     ctx->tb = t;
   }
   cudaStream_t s = ctx->s_main;
+  TRY(begin_timed(ctx));
   CU(cudaMemcpyAsync(ctx->node0[kPhi], phi0, sizeof(double) * n,
                      phi0_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-  std::vector<double> incs;
   for (int step = 0; step < o->n_steps; ++step) {
     TRY(do_initialize(ctx));
     cisdc_step_report rep{};
-    int k;
-    for (k = 1; k <= o->n_sweeps; ++k) {
-      const int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters);
-      int rc2 = rc;
-      const bool need_sync = o->has_stop_tol || k == o->n_sweeps || rc;
-      if (!rc) {
-        CU(cudaMemcpyAsync(ctx->h_incr, ctx->d_incr, sizeof(double), cudaMemcpyDeviceToHost, s));
-        if (need_sync) rc2 = check_status(ctx, &rep.counters, s);
+    int done = 0;
+    auto fail = [&](int rc) {
+      ctx->err = "integrate: step " + std::to_string(step + 1) + ", sweep " + std::to_string(done + 1) + ": " + ctx->err;
+      return rc == CISDC_E_CUDA ? rc : CISDC_E_SOLVE;
+    };
+    if (o->has_stop_tol) {
+      for (int k = 1; k <= o->n_sweeps; ++k) {
+        int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters, k - 1);
+        if (!rc) {
+          CU(cudaMemcpyAsync(ctx->h_incr + (k - 1), ctx->d_incr + (k - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
+          rc = check_status(ctx, &rep.counters);
+        }
+        if (rc) return fail(rc);
+        done = k;
+        if (ctx->h_incr[k - 1] <= o->stop_tol) break;
       }
-      if (rc2) {
-        ctx->err = "integrate: step " + std::to_string(step + 1) + ", sweep " + std::to_string(k) + ": " + ctx->err;
-        return rc2 == CISDC_E_CUDA ? rc2 : CISDC_E_SOLVE;
+    } else {
+      for (int k = 1; k <= o->n_sweeps; ++k) {
+        const int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters, k - 1);
+        if (rc) return fail(rc);
       }
-      if (!need_sync) CU(cudaStreamSynchronize(s));
-      const double inc = *ctx->h_incr;
-      if (increments) increments[(size_t)step * o->n_sweeps + (k - 1)] = inc;
-      ctx->last_incr = inc;
-      ctx->have_incr = true;
-      if (o->has_stop_tol && inc <= o->stop_tol) {
-        ++k;
-        break;
+      CU(cudaMemcpyAsync(ctx->h_incr, ctx->d_incr, sizeof(double) * o->n_sweeps, cudaMemcpyDeviceToHost, s));
+      const int rc = check_status(ctx, &rep.counters);
+      if (rc) {
+        ctx->err = "integrate: step " + std::to_string(step + 1) + ": " + ctx->err;
+        return rc == CISDC_E_CUDA ? rc : CISDC_E_SOLVE;
       }
+      done = o->n_sweeps;
     }
-    rep.sweeps = k - 1;
+    for (int k = 0; k < done; ++k)
+      if (increments) increments[(size_t)step * o->n_sweeps + k] = ctx->h_incr[k];
+    ctx->last_incr = ctx->h_incr[done - 1];
+    ctx->have_incr = true;
+    rep.sweeps = done;
     if (reports) reports[step] = rep;
-    // start = state.phi[M]: becomes node 0 of the next step
-    CU(cudaMemcpyAsync(ctx->scratch, V(ctx, ctx->cur, kPhi, ctx->M), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
-    CU(cudaMemcpyAsync(ctx->node0[kPhi], ctx->scratch, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    // start = state.phi[M] becomes node 0 of the next step
+    CU(cudaMemcpyAsync(ctx->node0[kPhi], V(ctx, ctx->cur, kPhi, ctx->M), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   }
   CU(cudaMemcpyAsync(final_state, ctx->node0[kPhi], sizeof(double) * n,
                      final_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
+  TRY(end_timed(ctx));
   return CISDC_OK;
 }
 
@@ -991,11 +1109,72 @@ int cisdc_gpu_integrate_device(cisdc_gpu_ctx* ctx, const double* d_phi0, size_t 
   return integrate_impl(ctx, d_phi0, true, n, opt, d_final_state, true, reports, increments);
 }
 
-int cisdc_gpu_kernel_times(cisdc_gpu_ctx* ctx, double* ms, int enable) {
-  (void)ctx;
-  (void)ms;
-  (void)enable;
-  return 0;
+int cisdc_gpu_set_timing(cisdc_gpu_ctx* ctx, int on) {
+  TRY(check_ctx(ctx));
+  ctx->tm.on = on != 0;
+  return CISDC_OK;
+}
+
+int cisdc_gpu_kernel_times(cisdc_gpu_ctx* ctx, double* ms, double* bytes, long long* launches, int max_classes,
+                           int reset) {
+  if (!ctx) return 0;
+  const int nc = std::min<int>(max_classes, kNumKernelClasses);
+  for (int c = 0; c < nc; ++c) {
+    if (ms) ms[c] = ctx->tm.ms[c];
+    if (bytes) bytes[c] = ctx->tm.bytes[c];
+    if (launches) launches[c] = ctx->tm.count[c];
+  }
+  if (reset) {
+    ctx->tm.reset();
+    ctx->device_ms = 0.0;
+  }
+  return nc;
+}
+
+const char* cisdc_gpu_kernel_class_name(int cls) {
+  return (cls >= 0 && cls < kNumKernelClasses) ? kClassNames[cls] : "?";
+}
+
+double cisdc_gpu_device_time_ms(cisdc_gpu_ctx* ctx, int reset) {
+  if (!ctx) return 0.0;
+  const double t = ctx->device_ms;
+  if (reset) ctx->device_ms = 0.0;
+  return t;
+}
+
+int cisdc_gpu_fp64_peak(double* tflops_dfma, double* tflops_dmul_dadd) {
+  cisdc_gpu_ctx* ctx = nullptr;  // for the CU() macro's error path
+  int dev = 0, sms = 0;
+  CU(cudaGetDevice(&dev));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* out = nullptr;
+  CU(cudaMalloc(&out, sizeof(double)));
+  cudaEvent_t a, b;
+  CU(cudaEventCreate(&a));
+  CU(cudaEventCreate(&b));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  const double ops = (double)blocks * threads * iters * 8;  // instructions (chains x iterations)
+  for (int variant = 0; variant < 2; ++variant) {
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+      CU(cudaEventRecord(a));
+      if (variant == 0) k_peak_dfma<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+      else k_peak_dmul_dadd<<<blocks, threads>>>(out, iters, 0.999999, 1e-7);
+      CU(cudaEventRecord(b));
+      CU(cudaEventSynchronize(b));
+      float t = 0.f;
+      CU(cudaEventElapsedTime(&t, a, b));
+      best = std::min(best, t);
+    }
+    // DFMA: 2 flops per instruction; DMUL+DADD: 2 instructions per 2 flops
+    const double tf = (variant == 0 ? 2.0 * ops : 2.0 * ops) / (best * 1e-3) / 1e12;
+    if (variant == 0 && tflops_dfma) *tflops_dfma = tf;
+    if (variant == 1 && tflops_dmul_dadd) *tflops_dmul_dadd = tf;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  return CISDC_OK;
 }
 
 }  // extern "C"

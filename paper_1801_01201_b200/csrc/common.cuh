@@ -46,6 +46,29 @@ struct Ops {
   double rd_cadv, rd_cdiff, rd_w[2][5];
 };
 
+// Kernel classes for the live per-class CUDA-event timing (cisdc_gpu_kernel_times).
+enum KernelClass {
+  kKQuad = 0,      // k_quad_base
+  kKRhs = 1,       // k_rhs
+  kKSolve1d = 2,   // k_solve1d_periodic / k_rd_banded_solve
+  kKMgSmooth = 3,  // k_mg_smooth
+  kKMgRestrict = 4,
+  kKMgProlong = 5,
+  kKMgNorm = 6,    // k_mg_absmax / k_mg_resmax / k_mg_update
+  kKReact = 7,     // k_react (Newton)
+  kKEvalAD = 8,    // k_eval_ad
+  kKEvalR = 9,     // k_eval_r
+  kKIncr = 10,     // k_incr_*
+  kNumKernelClasses = 11
+};
+
+// Called around every kernel launch (timing is a no-op unless enabled).
+struct LaunchHook {
+  virtual void before(int cls, cudaStream_t s) = 0;
+  virtual void after(int cls, cudaStream_t s, double bytes) = 0;
+  virtual ~LaunchHook() = default;
+};
+
 __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
 __device__ __forceinline__ double face_u(const Ops& o, int a, int i, int j, int k) {

@@ -312,7 +312,7 @@ struct MgRunner {
   const cisdc_problem_desc& d;
   MgCoef C[kMgMaxLevels];
   cudaStream_t s;
-  long long* launches;
+  LaunchHook* hook;
   // level-0 x lives in h.lv[0].x (ping-pong with .t); b0 = rhs
   const double* b0;
 
@@ -321,9 +321,10 @@ struct MgRunner {
 
   void smooth(int l, bool from_zero) {
     MgLevel& L = h.lv[l];
+    hook->before(kKMgSmooth, s);
     k_mg_smooth<DIM><<<grid(L.ncell), 256, 0, s>>>(C[l], L.x, bof(l), L.t, L.nx, L.ny, L.nz, from_zero ? 1 : 0,
                                                    h.d_active);
-    ++*launches;
+    hook->after(kKMgSmooth, s, 8.0 * L.ncell * h.S * (from_zero ? 2 : 3));
     std::swap(L.x, L.t);
   }
   void vcycle(int l) {
@@ -334,25 +335,27 @@ struct MgRunner {
     }
     for (int it = 0; it < d.mg_pre; ++it) smooth(l, l > 0 && it == 0);
     MgLevel& Cl = h.lv[l + 1];
+    hook->before(kKMgRestrict, s);
     k_mg_restrict<DIM><<<grid(Cl.ncell), 256, 0, s>>>(C[l], L.x, bof(l), L.nx, L.ny, L.nz, Cl.b, Cl.nx, Cl.ny, Cl.nz,
                                                       h.d_active);
-    ++*launches;
+    hook->after(kKMgRestrict, s, 8.0 * h.S * (2.0 * L.ncell + Cl.ncell));
     vcycle(l + 1);
+    hook->before(kKMgProlong, s);
     k_mg_prolong<DIM><<<grid(L.ncell), 256, 0, s>>>(L.x, L.nx, L.ny, L.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
-    ++*launches;
+    hook->after(kKMgProlong, s, 8.0 * h.S * (2.0 * L.ncell + Cl.ncell));
     for (int it = 0; it < d.mg_post; ++it) smooth(l, false);
   }
 };
 
 template <int DIM>
 inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
-                        double* out, DevStatus* st, cudaStream_t s, long long* launches) {
+                        double* out, DevStatus* st, cudaStream_t s, LaunchHook* hook) {
   const long long n = g.n;
   if (coef == 0.0) {
     if (cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
     return CISDC_OK;
   }
-  MgRunner<DIM> R{h, d, {}, s, launches, rhs};
+  MgRunner<DIM> R{h, d, {}, s, hook, rhs};
   for (int l = 0; l < h.L; ++l) R.C[l] = mg_coef(d, l, coef);
   std::vector<int> ones(g.S, 1);
   cudaMemcpyAsync(h.d_active, ones.data(), sizeof(int) * g.S, cudaMemcpyHostToDevice, s);
@@ -363,13 +366,17 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   MgLevel& L0 = h.lv[0];
   cudaMemcpyAsync(L0.x, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);  // x = b
   const dim3 rgrid((unsigned)std::min<long long>((g.ncell + 255) / 256, 1184), (unsigned)g.S, 1);
+  hook->before(kKMgNorm, s);
   k_mg_absmax<<<rgrid, 256, 0, s>>>(rhs, g.ncell, h.d_bmax);
-  *launches += 1;
+  hook->after(kKMgNorm, s, 8.0 * n);
   for (;;) {
+    hook->before(kKMgNorm, s);
     k_mg_resmax<DIM><<<rgrid, 256, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
+    hook->after(kKMgNorm, s, 16.0 * n);
+    hook->before(kKMgNorm, s);
     k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax, h.d_flag,
                                  st);
-    *launches += 2;
+    hook->after(kKMgNorm, s, 0.0);
     cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
     if (!h.h_flag[0]) break;
@@ -381,11 +388,11 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
 }
 
 inline int mg_solve(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
-                    double* out, DevStatus* st, cudaStream_t s, long long* launches) {
+                    double* out, DevStatus* st, cudaStream_t s, LaunchHook* hook) {
   switch (g.ndim) {
-    case 1: return mg_solve_dim<1>(h, g, d, coef, rhs, out, st, s, launches);
-    case 2: return mg_solve_dim<2>(h, g, d, coef, rhs, out, st, s, launches);
-    default: return mg_solve_dim<3>(h, g, d, coef, rhs, out, st, s, launches);
+    case 1: return mg_solve_dim<1>(h, g, d, coef, rhs, out, st, s, hook);
+    case 2: return mg_solve_dim<2>(h, g, d, coef, rhs, out, st, s, hook);
+    default: return mg_solve_dim<3>(h, g, d, coef, rhs, out, st, s, hook);
   }
 }
 
