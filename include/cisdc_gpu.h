@@ -29,7 +29,9 @@
 #ifndef CISDC_GPU_H_
 #define CISDC_GPU_H_
 
+#ifndef __CUDACC_RTC__
 #include <stddef.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -153,6 +155,7 @@ typedef struct cisdc_step_report {
   cisdc_counters counters;
 } cisdc_step_report;
 
+#ifndef __CUDACC_RTC__ /* device-side runtime compilation sees only the types above */
 typedef struct cisdc_gpu_ctx cisdc_gpu_ctx;
 
 int cisdc_make_quadrature_tables(int M, int convention, cisdc_tables* out);
@@ -199,6 +202,11 @@ double cisdc_gpu_device_time_ms(cisdc_gpu_ctx* ctx, int reset);
 long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx);
 /* FP64 pipe peak on the current device: DFMA chains and DMUL+DADD chains, TFLOP/s */
 int cisdc_gpu_fp64_peak(double* tflops_dfma, double* tflops_dmul_dadd);
+/* Generate and NVRTC-compile the network-specialised Newton kernels of a mass-action problem for
+   sm_100a without loading them (no GPU needed); the compiler log goes to log[cap]. */
+int cisdc_rtc_compile_check(const cisdc_problem_desc* desc, char* log, size_t cap);
+
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

@@ -177,8 +177,9 @@ int co_problem_create(const cisdc_problem_desc* desc, co_problem** out, char* er
         p->mg_b[l] = (double*)calloc(nc, sizeof(double));
         p->mg_t[l] = (double*)calloc(nc, sizeof(double));
       }
-      if (desc->mg_pre < 1 || desc->mg_coarse_sweeps < 1 || desc->mg_post < 0 || desc->mg_max_cycles < 1)
-        BAD("multigrid: need mg_pre >= 1, mg_coarse_sweeps >= 1, mg_max_cycles >= 1");
+      if (desc->mg_pre < 2 || desc->mg_coarse_sweeps < 2 || desc->mg_post < 0 || desc->mg_max_cycles < 1 ||
+          desc->mg_pre % 2 || desc->mg_post % 2 || desc->mg_coarse_sweeps % 2)
+        BAD("multigrid: need even mg_pre >= 2, mg_post >= 0, mg_coarse_sweeps >= 2 and mg_max_cycles >= 1");
     } else {
       BAD("unknown diffusion solver");
     }
@@ -693,8 +694,8 @@ static int adr_solve_diffusion_scan(co_problem* p, double coef, const double* rh
  * with identical per-point arithmetic:
  *   level l: n_l = n >> l per active axis, h_l = h * 2^l, c_la = d / (12 h_l h_l)
  *   A x   = x - coef * lap,  lap = sum_a c_la * stencil_a(x)   (stencil as Lap4 above)
- *   Jacobi: x' = x + wD * (b - A x), wD = omega / (1 + coef * (30 * sum_a c_la));
- *           from a zero guess x' = wD * b
+ *   Jacobi: x' = x + wD * (b - A x), wD from the spectral plan (mg_plan below);
+ *           from a zero guess x' = wD * b; levels used per solve = mg_plan's L
  *   restriction: mean of the 2^ndim children of (b - A x), summed x-fastest then y then z
  *   prolongation: cell-centred (bi/tri)linear, 3/4-1/4 per axis, x then y then z, periodic
  *   V-cycle: pre-smooth (first from zero below the top), restrict, recurse, correct, post-smooth;
@@ -824,19 +825,52 @@ static void mg_vcycle(co_problem* p, mg_level_op* ops, int l) {
   for (int it = 0; it < d->mg_post; ++it) mg_smooth(&ops[l], b, x, t, 0);
 }
 
-void co_mg_level_coeffs(const cisdc_problem_desc* d, int l, int s, double coef, double* c3, double* wD) {
-  double csum = 0.0;
-  for (int a = 0; a < 3; ++a) c3[a] = 0.0;
-  for (int a = 0; a < d->ndim; ++a) {
-    const double hl = d->h[a] * (double)(1 << l);
-    c3[a] = d->diffusivity[s] / (12.0 * hl * hl);
-    csum = csum + c3[a];
+/* Per-solve multigrid plan (csrc/multigrid.cuh mg_plan does the same arithmetic):
+ *   A_l = I - coef F_D,l has spectrum [1, Emax], Emax = 1 + coef * 64 * sum_a c_la; the modes that are
+ *   high-frequency in some axis sit above Ehf = 1 + coef * 28 * min_a c_la.
+ *   Weighted Jacobi with the optimal weight for the targeted interval [Elo, Emax]:
+ *     wD = 2 / (Elo + Emax),  Elo = Ehf on levels that hand the smooth modes to a coarser grid,
+ *                             Elo = 1 on the coarsest level used (it must reduce every mode).
+ *   Coarsen below level l only while the level is stiff: (Emax - 1) / (Emax + 1) > 0.1 for the
+ *   stiffest species (a well-conditioned level is solved by its own sweeps; a near-identity
+ *   system -- small coef d / h^2 -- uses no coarse grid at all).
+ *   The coarsest level does mg_coarse_sweeps sweeps, or mg_pre sweeps when it is the only level. */
+static int mg_plan(const co_problem* p, double coef, double wD[MAXL][MAXS], double c3[MAXL][MAXS][3]) {
+  const cisdc_problem_desc* d = &p->d;
+  double rho[MAXL];
+  double emax[MAXL][MAXS], ehf[MAXL][MAXS];
+  for (int l = 0; l < p->L; ++l) {
+    rho[l] = 0.0;
+    for (int s = 0; s < p->S; ++s) {
+      double csum = 0.0, cmin = 0.0;
+      for (int a = 0; a < 3; ++a) c3[l][s][a] = 0.0;
+      for (int a = 0; a < d->ndim; ++a) {
+        const double hl = d->h[a] * (double)(1 << l);
+        c3[l][s][a] = d->diffusivity[s] / (12.0 * hl * hl);
+        csum = csum + c3[l][s][a];
+        cmin = (a == 0 || c3[l][s][a] < cmin) ? c3[l][s][a] : cmin;
+      }
+      emax[l][s] = 1.0 + coef * (64.0 * csum);
+      ehf[l][s] = 1.0 + coef * (28.0 * cmin);
+      const double r = (emax[l][s] - 1.0) / (emax[l][s] + 1.0);
+      rho[l] = r > rho[l] ? r : rho[l];
+    }
   }
-  *wD = d->mg_omega / (1.0 + coef * (30.0 * csum));
+  int L = 1;
+  while (L < p->L && rho[L - 1] > 0.1) ++L;
+  for (int l = 0; l < L; ++l)
+    for (int s = 0; s < p->S; ++s) wD[l][s] = 2.0 / ((l < L - 1 ? ehf[l][s] : 1.0) + emax[l][s]);
+  return L;
 }
 
 static int adr_solve_diffusion_mg(co_problem* p, double coef, const double* rhs, double* out, cisdc_counters* c) {
   const size_t nc = p->ncell;
+  double wD[MAXL][MAXS], c3[MAXL][MAXS][3];
+  const int Lsave = p->L;
+  const int Luse = coef == 0.0 ? 1 : mg_plan(p, coef, wD, c3);
+  const int coarse_save = p->d.mg_coarse_sweeps;
+  p->L = Luse;
+  if (Luse == 1) p->d.mg_coarse_sweeps = p->d.mg_pre;
   for (int s = 0; s < p->S; ++s) {
     const double* b = rhs + (size_t)s * nc;
     double* o = out + (size_t)s * nc;
@@ -845,13 +879,14 @@ static int adr_solve_diffusion_mg(co_problem* p, double coef, const double* rhs,
       continue;
     }
     mg_level_op ops[MAXL];
-    for (int l = 0; l < p->L; ++l) {
+    for (int l = 0; l < Luse; ++l) {
       ops[l].nx = p->ln[l][0];
       ops[l].ny = p->ln[l][1];
       ops[l].nz = p->ln[l][2];
       ops[l].ndim = p->d.ndim;
       ops[l].coef = coef;
-      co_mg_level_coeffs(&p->d, l, s, coef, ops[l].c, &ops[l].wD);
+      for (int a = 0; a < 3; ++a) ops[l].c[a] = c3[l][s][a];
+      ops[l].wD = wD[l][s];
     }
     double bn = 0.0;
     for (size_t i = 0; i < nc; ++i)
@@ -867,6 +902,8 @@ static int adr_solve_diffusion_mg(co_problem* p, double coef, const double* rhs,
         snprintf(p->err, sizeof(p->err),
                  "solve_diffusion: multigrid: species %d: no convergence in %d cycles (residual %.3e, target %.3e)",
                  s, cyc, rn, thr);
+        p->L = Lsave;
+        p->d.mg_coarse_sweeps = coarse_save;
         return CISDC_E_NUMERIC;
       }
       mg_vcycle(p, ops, 0);
@@ -875,6 +912,8 @@ static int adr_solve_diffusion_mg(co_problem* p, double coef, const double* rhs,
     if (c) c->mg_cycles += cyc;
     memcpy(o, p->mg_x[0], sizeof(double) * nc);
   }
+  p->L = Lsave;
+  p->d.mg_coarse_sweeps = coarse_save;
   return CISDC_OK;
 }
 

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -24,6 +25,7 @@
 #include "newton.cuh"
 #include "peak.cuh"
 #include "pointwise.cuh"
+#include "rtc.cuh"
 #include "solve1d.cuh"
 #include "stencil.cuh"
 
@@ -129,6 +131,7 @@ struct cisdc_gpu_ctx {
   // solvers
   double* rd_work = nullptr;
   MgHierarchy mg;
+  RtcNewton rtc;  // network-specialised Newton kernels (mass action)
   // status / reductions
   DevStatus* d_st = nullptr;
   DevStatus* h_st = nullptr;  // pinned
@@ -273,6 +276,19 @@ int launch_react_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
 }
 
 int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t s) {
+  if (ctx->rtc.ready) {
+    Reaction rx = ctx->rx;
+    Ops o = ctx->ops;
+    Geom g = ctx->g;
+    ReactArgs aa = a;
+    DevStatus* st = ctx->d_st;
+    void* args[5] = {&rx, &o, &g, &aa, &st};
+    ctx->tm.before(kKReact, s);
+    CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)), dim3(128),
+                        args, 0, s));
+    ctx->tm.after(kKReact, s, F8(ctx) * react_fields(mode, a));
+    return CISDC_OK;
+  }
   switch (mode) {
     case kModeMisdcq: return launch_react_m<kModeMisdcq>(ctx, a, s);
     case kModeMisdc: return launch_react_m<kModeMisdc>(ctx, a, s);
@@ -678,6 +694,34 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
 
 int check_ctx(cisdc_gpu_ctx* ctx) { return ctx ? CISDC_OK : CISDC_E_INVALID_ARGUMENT; }
 
+// mass-action network of the descriptor -> Reaction (nu_sr = products - reactants)
+int fill_mass_action(const cisdc_problem_desc* d, Reaction& rx, std::string& why) {
+  const int S = d->nspecies;
+  if (d->n_reactions < 0 || d->n_reactions > kMaxR) {
+    why = "mass action: too many reactions";
+    return 1;
+  }
+  rx.nr = d->n_reactions;
+  for (int r = 0; r < rx.nr; ++r) {
+    for (int t = 0; t < 2; ++t) {
+      const int a = d->reactants[2 * r + t], p = d->products[2 * r + t];
+      if (a >= S || p >= S) {
+        why = "mass action: species index out of range";
+        return 1;
+      }
+      rx.reac[r][t] = (signed char)(a < 0 ? -1 : a);
+      if (a >= 0) rx.nu[a][r] -= 1;
+      if (p >= 0) rx.nu[p][r] += 1;
+    }
+    if (rx.reac[r][0] < 0) {
+      why = "mass action: every reaction needs a first reactant";
+      return 1;
+    }
+    rx.k[r] = d->rate_constants[r];
+  }
+  return 0;
+}
+
 int do_initialize(cisdc_gpu_ctx* ctx) {
   cudaStream_t s = ctx->s_main;
   TRY(launch_eval_ad(ctx, ctx->node0[kPhi], ctx->node0[kFa], ctx->node0[kFd], s));
@@ -736,6 +780,7 @@ void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
   cudaDeviceSynchronize();
   for (void* p : ctx->allocs) cudaFree(p);
   mg_free(ctx->mg);
+  rtc_free(ctx->rtc);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   if (ctx->h_incr) cudaFreeHost(ctx->h_incr);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
@@ -822,20 +867,12 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     if (d->reaction_kind == CISDC_REACTION_LINEAR_DECAY || d->reaction_kind == CISDC_REACTION_BISTABLE) {
       if (S != 1) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "scalar reaction kinds need nspecies == 1");
     } else if (d->reaction_kind == CISDC_REACTION_MASS_ACTION) {
-      if (d->n_reactions < 0 || d->n_reactions > kMaxR)
-        return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: too many reactions");
-      rx.nr = d->n_reactions;
-      for (int r = 0; r < rx.nr; ++r) {
-        for (int t = 0; t < 2; ++t) {
-          const int a = d->reactants[2 * r + t], p = d->products[2 * r + t];
-          if (a >= S || p >= S) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: species index out of range");
-          rx.reac[r][t] = (signed char)(a < 0 ? -1 : a);
-          if (a >= 0) rx.nu[a][r] -= 1;
-          if (p >= 0) rx.nu[p][r] += 1;
-        }
-        if (rx.reac[r][0] < 0)
-          return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "mass action: every reaction needs a first reactant");
-        rx.k[r] = d->rate_constants[r];
+      std::string why;
+      if (fill_mass_action(d, rx, why)) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, why);
+      const char* env = std::getenv("CISDC_RTC");
+      if (!(env && env[0] == '0')) {
+        if (rtc_build(ctx->rtc, rx, S, d->ndim, true))
+          return set_err(ctx, CISDC_E_CUDA, "NVRTC network kernel build failed:\n" + ctx->rtc.log);
       }
     } else if (d->reaction_kind != CISDC_REACTION_NONE) {
       return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown reaction kind");
@@ -1129,6 +1166,21 @@ int cisdc_gpu_kernel_times(cisdc_gpu_ctx* ctx, double* ms, double* bytes, long l
     ctx->device_ms = 0.0;
   }
   return nc;
+}
+
+int cisdc_rtc_compile_check(const cisdc_problem_desc* d, char* log, size_t cap) {
+  if (!d || d->reaction_kind != CISDC_REACTION_MASS_ACTION) return CISDC_E_INVALID_ARGUMENT;
+  Reaction rx{};
+  std::string why;
+  if (fill_mass_action(d, rx, why)) {
+    if (log && cap) std::snprintf(log, cap, "%s", why.c_str());
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  rx.kind = CISDC_REACTION_MASS_ACTION;
+  RtcNewton r;
+  const int rc = rtc_build(r, rx, d->nspecies, d->ndim, false);
+  if (log && cap) std::snprintf(log, cap, "%s", (rc ? r.log : std::string("ok\n") + r.log).c_str());
+  return rc;
 }
 
 const char* cisdc_gpu_kernel_class_name(int cls) {

@@ -5,8 +5,10 @@
 // results are bit-identical to the CPU oracle / the reference's no-FMA x86-64 build.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+#endif
 
 #include "../../include/cisdc_gpu.h"
 
@@ -62,12 +64,14 @@ enum KernelClass {
   kNumKernelClasses = 11
 };
 
+#ifndef __CUDACC_RTC__
 // Called around every kernel launch (timing is a no-op unless enabled).
 struct LaunchHook {
   virtual void before(int cls, cudaStream_t s) = 0;
   virtual void after(int cls, cudaStream_t s, double bytes) = 0;
   virtual ~LaunchHook() = default;
 };
+#endif
 
 __device__ __forceinline__ int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
@@ -83,6 +87,8 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
   atomicMax(reinterpret_cast<unsigned long long*>(addr), __double_as_longlong(v));
 }
 
+#ifndef __CUDACC_RTC__
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+#endif
 
 }  // namespace cisdc_b200

@@ -15,6 +15,8 @@
 //   k_mg_prolong   (bi/tri)linear cell-centred interpolation + correction, fused
 #pragma once
 
+#include <algorithm>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -41,6 +43,7 @@ struct MgHierarchy {
   double* d_rmax = nullptr;       // [S]
   int* d_flag = nullptr;          // [2]: any_active, failed species + 1
   int* h_flag = nullptr;          // pinned mirror
+  std::vector<std::pair<double, int>> predicted;  // cycles the last solve with this coef needed
   std::vector<void*> allocs;
 };
 
@@ -243,7 +246,9 @@ inline int mg_init(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d) {
   h.S = g.S;
   int n[3] = {g.nx, g.ny, g.nz};
   const int minc = d.mg_min_coarse > 2 ? d.mg_min_coarse : 4;
-  if (d.mg_pre < 1 || d.mg_coarse_sweeps < 1 || d.mg_post < 0 || d.mg_max_cycles < 1) return CISDC_E_INVALID_ARGUMENT;
+  if (d.mg_pre < 2 || d.mg_coarse_sweeps < 2 || d.mg_post < 0 || d.mg_max_cycles < 1 || d.mg_pre % 2 ||
+      d.mg_post % 2 || d.mg_coarse_sweeps % 2)
+    return CISDC_E_INVALID_ARGUMENT;  // even sweep counts: see MgRunner
   h.L = 0;
   for (;;) {
     MgLevel& L = h.lv[h.L];
@@ -290,20 +295,35 @@ inline void mg_free(MgHierarchy& h) {
   h.h_flag = nullptr;
 }
 
-inline MgCoef mg_coef(const cisdc_problem_desc& d, int l, double coef) {
-  MgCoef C{};
-  C.ndim = d.ndim;
-  C.coef = coef;
-  for (int s = 0; s < d.nspecies; ++s) {
-    double csum = 0.0;
-    for (int a = 0; a < d.ndim; ++a) {
-      const double hl = d.h[a] * (double)(1 << l);
-      C.c[s][a] = d.diffusivity[s] / (12.0 * hl * hl);
-      csum = csum + C.c[s][a];
+// Per-solve plan: levels used and optimal Jacobi weights (identical arithmetic to the oracle's
+// mg_plan, oracle/co_problems.c).  Returns the number of levels used.
+inline int mg_plan(const MgHierarchy& h, const cisdc_problem_desc& d, double coef, MgCoef* C) {
+  double rho[kMgMaxLevels];
+  double emax[kMgMaxLevels][kMaxS], ehf[kMgMaxLevels][kMaxS];
+  for (int l = 0; l < h.L; ++l) {
+    C[l] = MgCoef{};
+    C[l].ndim = d.ndim;
+    C[l].coef = coef;
+    rho[l] = 0.0;
+    for (int s = 0; s < d.nspecies; ++s) {
+      double csum = 0.0, cmin = 0.0;
+      for (int a = 0; a < d.ndim; ++a) {
+        const double hl = d.h[a] * (double)(1 << l);
+        C[l].c[s][a] = d.diffusivity[s] / (12.0 * hl * hl);
+        csum = csum + C[l].c[s][a];
+        cmin = (a == 0 || C[l].c[s][a] < cmin) ? C[l].c[s][a] : cmin;
+      }
+      emax[l][s] = 1.0 + coef * (64.0 * csum);
+      ehf[l][s] = 1.0 + coef * (28.0 * cmin);
+      const double r = (emax[l][s] - 1.0) / (emax[l][s] + 1.0);
+      rho[l] = r > rho[l] ? r : rho[l];
     }
-    C.wD[s] = d.mg_omega / (1.0 + coef * (30.0 * csum));
   }
-  return C;
+  int L = 1;
+  while (L < h.L && rho[L - 1] > 0.1) ++L;
+  for (int l = 0; l < L; ++l)
+    for (int s = 0; s < d.nspecies; ++s) C[l].wD[s] = 2.0 / ((l < L - 1 ? ehf[l][s] : 1.0) + emax[l][s]);
+  return L;
 }
 
 template <int DIM>
@@ -311,38 +331,41 @@ struct MgRunner {
   MgHierarchy& h;
   const cisdc_problem_desc& d;
   MgCoef C[kMgMaxLevels];
+  int L;  // levels used by this solve
   cudaStream_t s;
   LaunchHook* hook;
-  // level-0 x lives in h.lv[0].x (ping-pong with .t); b0 = rhs
+  // level-0 x lives in h.lv[0].x (ping-pong with .t); b0 = rhs.  Sweep counts are even, so after
+  // every pair of sweeps .x holds the iterate again for active AND masked (converged) species.
   const double* b0;
 
   const double* bof(int l) const { return l == 0 ? b0 : h.lv[l].b; }
   dim3 grid(long long ncell) const { return dim3((unsigned)((ncell + 255) / 256), (unsigned)h.S, 1); }
 
   void smooth(int l, bool from_zero) {
-    MgLevel& L = h.lv[l];
+    MgLevel& Lv = h.lv[l];
     hook->before(kKMgSmooth, s);
-    k_mg_smooth<DIM><<<grid(L.ncell), 256, 0, s>>>(C[l], L.x, bof(l), L.t, L.nx, L.ny, L.nz, from_zero ? 1 : 0,
-                                                   h.d_active);
-    hook->after(kKMgSmooth, s, 8.0 * L.ncell * h.S * (from_zero ? 2 : 3));
-    std::swap(L.x, L.t);
+    k_mg_smooth<DIM><<<grid(Lv.ncell), 256, 0, s>>>(C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
+                                                    h.d_active);
+    hook->after(kKMgSmooth, s, 8.0 * Lv.ncell * h.S * (from_zero ? 2 : 3));
+    std::swap(Lv.x, Lv.t);
   }
   void vcycle(int l) {
-    MgLevel& L = h.lv[l];
-    if (l == h.L - 1) {
-      for (int it = 0; it < d.mg_coarse_sweeps; ++it) smooth(l, l > 0 && it == 0);
+    MgLevel& Lv = h.lv[l];
+    if (l == L - 1) {
+      const int ns = L == 1 ? d.mg_pre : d.mg_coarse_sweeps;
+      for (int it = 0; it < ns; ++it) smooth(l, l > 0 && it == 0);
       return;
     }
     for (int it = 0; it < d.mg_pre; ++it) smooth(l, l > 0 && it == 0);
     MgLevel& Cl = h.lv[l + 1];
     hook->before(kKMgRestrict, s);
-    k_mg_restrict<DIM><<<grid(Cl.ncell), 256, 0, s>>>(C[l], L.x, bof(l), L.nx, L.ny, L.nz, Cl.b, Cl.nx, Cl.ny, Cl.nz,
-                                                      h.d_active);
-    hook->after(kKMgRestrict, s, 8.0 * h.S * (2.0 * L.ncell + Cl.ncell));
+    k_mg_restrict<DIM><<<grid(Cl.ncell), 256, 0, s>>>(C[l], Lv.x, bof(l), Lv.nx, Lv.ny, Lv.nz, Cl.b, Cl.nx, Cl.ny,
+                                                      Cl.nz, h.d_active);
+    hook->after(kKMgRestrict, s, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell));
     vcycle(l + 1);
     hook->before(kKMgProlong, s);
-    k_mg_prolong<DIM><<<grid(L.ncell), 256, 0, s>>>(L.x, L.nx, L.ny, L.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
-    hook->after(kKMgProlong, s, 8.0 * h.S * (2.0 * L.ncell + Cl.ncell));
+    k_mg_prolong<DIM><<<grid(Lv.ncell), 256, 0, s>>>(Lv.x, Lv.nx, Lv.ny, Lv.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
+    hook->after(kKMgProlong, s, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell));
     for (int it = 0; it < d.mg_post; ++it) smooth(l, false);
   }
 };
@@ -355,8 +378,8 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     if (cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
     return CISDC_OK;
   }
-  MgRunner<DIM> R{h, d, {}, s, hook, rhs};
-  for (int l = 0; l < h.L; ++l) R.C[l] = mg_coef(d, l, coef);
+  MgRunner<DIM> R{h, d, {}, 1, s, hook, rhs};
+  R.L = mg_plan(h, d, coef, R.C);
   std::vector<int> ones(g.S, 1);
   cudaMemcpyAsync(h.d_active, ones.data(), sizeof(int) * g.S, cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(h.d_cycles, 0, sizeof(int) * g.S, s);
@@ -369,18 +392,48 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   hook->before(kKMgNorm, s);
   k_mg_absmax<<<rgrid, 256, 0, s>>>(rhs, g.ncell, h.d_bmax);
   hook->after(kKMgNorm, s, 8.0 * n);
+  // The host enqueues cycles in batches (predicted from the last solve with this coefficient) and
+  // only then looks at the device flag: cycles past convergence are masked no-ops, so the result
+  // is identical to checking after every cycle.
+  int batch = 1;
+  for (const auto& pc : h.predicted)
+    if (pc.first == coef) batch = std::max(1, pc.second);
+  int launched = 0;
   for (;;) {
-    hook->before(kKMgNorm, s);
-    k_mg_resmax<DIM><<<rgrid, 256, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
-    hook->after(kKMgNorm, s, 16.0 * n);
-    hook->before(kKMgNorm, s);
-    k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax, h.d_flag,
-                                 st);
-    hook->after(kKMgNorm, s, 0.0);
+    for (int b = 0; b < batch; ++b) {
+      hook->before(kKMgNorm, s);
+      k_mg_resmax<DIM><<<rgrid, 256, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
+      hook->after(kKMgNorm, s, 16.0 * n);
+      hook->before(kKMgNorm, s);
+      k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
+                                   h.d_flag, st);
+      hook->after(kKMgNorm, s, 0.0);
+      if (launched + b < d.mg_max_cycles) R.vcycle(0);
+    }
+    launched += batch;
     cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
-    if (!h.h_flag[0]) break;
-    R.vcycle(0);
+    if (!h.h_flag[0] || h.h_flag[1] || launched > d.mg_max_cycles) break;
+    batch = 1;
+  }
+  // remember how many cycles this coefficient needed (flag[0] == 0 after the last check)
+  int used = launched;
+  {
+    std::vector<int> cyc(g.S);
+    cudaMemcpy(cyc.data(), h.d_cycles, sizeof(int) * g.S, cudaMemcpyDeviceToHost);
+    used = 0;
+    for (int v : cyc) used = std::max(used, v);
+    used = std::max(used, 1);
+  }
+  bool found = false;
+  for (auto& pc : h.predicted)
+    if (pc.first == coef) {
+      pc.second = used;
+      found = true;
+    }
+  if (!found) {
+    if (h.predicted.size() >= 64) h.predicted.erase(h.predicted.begin());
+    h.predicted.push_back({coef, used});
   }
   if (cudaMemcpyAsync(out, L0.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
   if (cudaGetLastError() != cudaSuccess) return CISDC_E_CUDA;

@@ -216,7 +216,8 @@ def config_c0(n_x: int = 200, a: float = 1.0, d: float = 2.0, r: float = 4.0, dt
                     ref_a=a, ref_d=d, ref_r=r, name="c0-reference-rd")
     dx = 20.0 / n_x
     x = (np.arange(n_x) + 0.5) * dx
-    phi0 = 0.5 * (1.0 + np.tanh(20.0 - 2.0 * x))  # initial_condition, reaction_diffusion.cpp:69-74
+    # initial_condition, reaction_diffusion.cpp:69-74 (libm tanh, like std::tanh)
+    phi0 = np.array([0.5 * (1.0 + math.tanh(20.0 - 2.0 * float(xi))) for xi in x])
     return RunSpec(p, phi0, 1, M, n_sweeps, dt, n_steps, name="c0", schemes=(0, 1, 2))
 
 

@@ -1,0 +1,274 @@
+"""GPU (native engine, through the C-ABI) against the CPU oracle and the unmodified reference.
+
+Bar (north_star): per-step max relative state difference <= 1e-10 with identical sweep and Newton
+iteration counts.  By construction (same operation order, no FMA) the engine is bit-identical to the
+oracle, so most checks assert array equality; the tolerance is asserted as well.
+"""
+import numpy as np
+import pytest
+
+from paper_1801_01201_b200 import _abi, api, problems as P
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def relerr(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def opts(spec, scheme, steps=None, nu=None, workers=0, conv=None, sweeps=None):
+    return api.IntegrateOptions(scheme=scheme, dt=spec.dt, n_steps=steps or spec.n_steps, M=spec.M,
+                                n_sweeps=sweeps or spec.n_sweeps, nu=nu or spec.nu, workers=workers,
+                                convention=spec.convention if conv is None else conv)
+
+
+def per_step_compare(oracle, spec, scheme, steps, nu=1, workers=0, conv=0):
+    """integrate step by step (n_steps = 1 fed back == one multi-step call, integrators.cpp:312-330)."""
+    ctx = api.GpuContext(spec.problem, spec.M, conv)
+    phi_g = spec.phi0.copy()
+    phi_c = spec.phi0.copy()
+    worst = 0.0
+    try:
+        for _ in range(steps):
+            o = opts(spec, scheme, steps=1, nu=nu, workers=workers, conv=conv)
+            g = api.integrate(spec.problem, phi_g, o, ctx=ctx)
+            c, reps, incs = oracle.integrate(spec.problem, phi_c, o)
+            worst = max(worst, relerr(g.final_state, c))
+            assert g.steps[0].sweeps == reps[0].sweeps
+            assert g.steps[0].counters.newton_iterations == reps[0].counters.newton_iterations
+            assert g.steps[0].counters.mg_cycles == reps[0].counters.mg_cycles
+            assert g.steps[0].counters.diffusion == reps[0].counters.diffusion
+            assert g.steps[0].counters.reaction == reps[0].counters.reaction
+            assert np.allclose(g.steps[0].increments, incs[: reps[0].sweeps], rtol=1e-12, atol=0)
+            phi_g, phi_c = g.final_state, c
+    finally:
+        ctx.close()
+    assert worst <= TOL
+    return worst, phi_g, phi_c
+
+
+# ------------------------------------------------------------------ config-0 gate: unmodified reference
+
+@pytest.mark.parametrize("scheme,nu,workers", [(0, 1, 0), (1, 1, 0), (2, 1, 0), (2, 3, 0), (2, 1, 2), (2, 3, 2)])
+@pytest.mark.parametrize("conv", [0, 1])
+def test_gate_reference_pde_bitwise(gpu, oracle, scheme, nu, workers, conv):
+    """The reference's own Dirichlet PDE (n_x = 200, a = 1, d = 2, r = 4): GPU == reference, bit for bit."""
+    spec = P.config_c0(n_steps=5)
+    o = opts(spec, scheme, steps=5, nu=nu, workers=workers, conv=conv)
+    g = api.integrate(spec.problem, spec.phi0, o)
+    if oracle.ref_lib() is not None:
+        r, reps, incs = oracle.ref_integrate(spec.problem, spec.phi0, o)
+    else:
+        r, reps, incs = oracle.integrate(spec.problem, spec.phi0, o)
+    assert np.array_equal(g.final_state, r)
+    for s, rep in zip(g.steps, reps):
+        assert s.sweeps == rep.sweeps
+        assert (s.counters.diffusion, s.counters.reaction) == (rep.counters.diffusion, rep.counters.reaction)
+    c, creps, _ = oracle.integrate(spec.problem, spec.phi0, o)
+    assert sum(s.counters.newton_iterations for s in g.steps) == sum(x.counters.newton_iterations for x in creps)
+
+
+# ------------------------------------------------------------------ BASELINE configs (scaled)
+
+CASES = {
+    "c1": (lambda: P.config_c1(), 10, (0, 1, 2)),
+    "c2": (lambda: P.config_c2(scale=16), 3, (0, 1, 2)),
+    "c3": (lambda: P.config_c3(scale=16, n_steps=1), 1, (0, 1, 2)),
+    "c4": (lambda: P.config_c4(scale=32, n_steps=1), 1, (0, 1, 2)),
+    "c5": (lambda: P.config_c5(scale=16), 1, (1, 2)),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_config_parity_per_step(gpu, oracle, name):
+    make, steps, schemes = CASES[name]
+    spec = make()
+    for scheme in schemes:
+        _, g, c = per_step_compare(oracle, spec, scheme, steps)
+        assert np.array_equal(g, c), f"{name} scheme {scheme}: not bitwise"
+
+
+def test_config1_full_run_both_schemes(gpu, oracle):
+    """C1 exactly as specified: N = 256, 100 steps, MISDC and PMISDC (CISDCQ nu = 1, concurrent)."""
+    spec = P.config_c1()
+    for scheme, workers in ((0, 0), (2, 2)):
+        o = opts(spec, scheme, workers=workers)
+        g = api.integrate(spec.problem, spec.phi0, o)
+        c, reps, _ = oracle.integrate(spec.problem, spec.phi0, o)
+        assert relerr(g.final_state, c) <= TOL
+        assert np.array_equal(g.final_state, c)
+        assert sum(s.counters.newton_iterations for s in g.steps) == sum(r.counters.newton_iterations for r in reps)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_pipelined_equals_serial_and_nested_iterations(gpu, oracle, name):
+    """execute_pipelined semantics: concurrent D/R streams == serial cell order, bitwise, nu = 1, 3."""
+    spec = CASES[name][0]()
+    for nu in (1, 3):
+        a = api.integrate(spec.problem, spec.phi0, opts(spec, 2, steps=1, nu=nu, workers=0))
+        b = api.integrate(spec.problem, spec.phi0, opts(spec, 2, steps=1, nu=nu, workers=2))
+        c, reps, _ = oracle.integrate(spec.problem, spec.phi0, opts(spec, 2, steps=1, nu=nu))
+        assert np.array_equal(a.final_state, b.final_state)
+        assert np.array_equal(a.final_state, c)
+        assert b.steps[0].counters.diffusion == nu * spec.M * spec.n_sweeps
+        assert b.steps[0].counters.newton_iterations == reps[0].counters.newton_iterations
+
+
+def test_full_size_config2_step(gpu, oracle):
+    """C2 at its full size (N = 65536, 5 nodes, 8 sweeps): two steps, all three schemes."""
+    spec = P.config_c2()
+    for scheme in (0, 1, 2):
+        per_step_compare(oracle, spec, scheme, 2)
+
+
+def test_1d_direct_solve_vs_independent_banded_lu(gpu, oracle):
+    """The GPU's exact circulant solve against the oracle's cyclic banded LU (reference banded_solve
+    semantics, an independent algorithm): agreement to round-off at C2 size and stiffness."""
+    spec = P.config_c2()
+    prob = api.GpuProblem(spec.problem, M=4)
+    desc_lu = P.config_c2().problem
+    desc_lu.diffusion_solver = _abi.DIFFUSION_BANDED_ORACLE
+    lu = oracle.Problem(desc_lu)
+    rng = np.random.default_rng(7)
+    rhs = spec.phi0 + 0.01 * rng.standard_normal(spec.phi0.size)
+    t = api.make_quadrature_tables(4)
+    for m in range(4):
+        coef = spec.dt * t.QtI[m, m]
+        x = prob.solve_diffusion(coef, rhs)
+        y = lu.solve(_abi.STAGE_DIFFUSION, coef, rhs)
+        assert relerr(x, y) <= 1e-12
+    prob.close()
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_stage_level_bitwise(gpu, oracle, name):
+    """OperatorSplitProblem stages one by one: eval_* and solve_* == oracle."""
+    spec = CASES[name][0]()
+    prob = api.GpuProblem(spec.problem, M=spec.M)
+    orc = oracle.Problem(spec.problem)
+    x = spec.phi0
+    for stage, fn in ((0, prob.eval_advection), (1, prob.eval_diffusion), (2, prob.eval_reaction)):
+        assert np.array_equal(fn(x), orc.eval(stage, x)), stage
+    coef = spec.dt * 0.3
+    c1, c2 = api.SolveCounters(), _abi.CountersC()
+    assert np.array_equal(prob.solve_diffusion(coef, x, c1), orc.solve(1, coef, x, c2))
+    assert np.array_equal(prob.solve_reaction(coef, x, c1), orc.solve(2, coef, x, c2))
+    assert c1.newton_iterations == c2.newton_iterations and c1.mg_cycles == c2.mg_cycles
+    # coef == 0 is the identity (reaction_diffusion.cpp:159)
+    assert np.array_equal(prob.solve_diffusion(0.0, x), x)
+    prob.close()
+
+
+def test_sweep_state_api(gpu, oracle):
+    """SweepState: initialize / set_node_values / run_sweep / fields / increment == oracle state."""
+    spec = P.config_c2(scale=64)
+    M = spec.M
+    rng = np.random.default_rng(3)
+    vals = np.stack([spec.phi0 + 0.01 * rng.standard_normal(spec.phi0.size) for _ in range(M + 1)])
+    st = api.SweepState(spec.problem, M)
+    st.set_node_values(vals)
+    fields, cnt = oracle.sweeps(spec.problem, M, 0, 1, spec.dt, 1, 3, values=vals)
+    cnt_g = api.SolveCounters()
+    prev = st.phi(M)
+    for _ in range(3):
+        api.run_sweep(api.Scheme.misdcq, st, spec.dt, 1, cnt_g)
+        inc = st.increment()
+        assert abs(inc - np.mean(np.abs(st.phi(M) - prev))) <= 1e-12 * max(inc, 1e-300)
+        prev = st.phi(M)
+    for w, get in enumerate((st.phi, st.fa, st.fd, st.fr, st.phi_ad)):
+        for m in range(M + 1):
+            if w == 4 and m == 0:
+                continue
+            assert np.array_equal(get(m), fields[w, m]), (w, m)
+    assert cnt_g.newton_iterations == cnt.newton_iterations
+    assert (cnt_g.diffusion, cnt_g.reaction) == (3 * M, 3 * M)
+    st.close()
+
+
+def test_newton_failure_reports_first_cell(gpu, oracle):
+    """A diverging undamped Newton (config-4 network at dt = 5e-4) raises SolveError naming the same
+    first failing cell as the oracle, with integrate's step/sweep context."""
+    spec = P.config_c4(scale=64, n_steps=1)
+    o = opts(spec, 1, steps=1)
+    o.dt = 5e-4
+    with pytest.raises(oracle.OracleError) as ce:
+        oracle.integrate(spec.problem, spec.phi0, o)
+    with pytest.raises(api.SolveError) as ge:
+        api.integrate(spec.problem, spec.phi0, o)
+    msg_c, msg_g = str(ce.value), str(ge.value)
+    assert "integrate: step 1" in msg_g and "cell" in msg_g
+    cell_c = msg_c.split("cell ")[1].split(":")[0]
+    cell_g = msg_g.split("cell ")[1].split(":")[0]
+    assert cell_c == cell_g
+
+
+def test_invalid_arguments(gpu):
+    spec = P.config_c1(scale=4)
+    with pytest.raises(ValueError):
+        api.integrate(spec.problem, spec.phi0, api.IntegrateOptions(n_sweeps=0))
+    with pytest.raises(ValueError):
+        api.integrate(spec.problem, spec.phi0, api.IntegrateOptions(scheme=2, nu=0, M=2, n_sweeps=1))
+    st = api.SweepState(spec.problem, 2)
+    st.initialize(spec.phi0)
+    with pytest.raises(api.CapabilityError):
+        api.run_sweep(api.Scheme.imexq, st, 1e-3)
+    with pytest.raises(ValueError):
+        st.initialize(np.zeros(3))
+    st.close()
+
+
+def test_run_to_run_determinism(gpu):
+    spec = P.config_c4(scale=32, n_steps=1)
+    o = opts(spec, 2, steps=1, workers=2)
+    a = api.integrate(spec.problem, spec.phi0, o).final_state
+    b = api.integrate(spec.problem, spec.phi0, o).final_state
+    assert np.array_equal(a, b)
+
+
+def test_multigrid_residual_property_full_size(gpu):
+    """C3 at full size (1024^2 x 3): the diffusion solve meets its residual tolerance and is linear."""
+    spec = P.config_c3()
+    prob = api.GpuProblem(spec.problem, M=spec.M)
+    coef = spec.dt * 0.3
+    x = prob.solve_diffusion(coef, spec.phi0)
+    # residual b - (x - coef F_D(x)) per species, inf-norm relative to ||b||
+    r = spec.phi0 - (x - coef * prob.eval_diffusion(x))
+    nc = spec.problem.ncell
+    for s in range(3):
+        assert np.max(np.abs(r[s * nc:(s + 1) * nc])) <= 1e-9 * np.max(np.abs(spec.phi0[s * nc:(s + 1) * nc]))
+    prob.close()
+
+
+def test_stop_tol_and_reports(gpu, oracle):
+    spec = P.config_c2(scale=64)
+    o = opts(spec, 1, steps=3, sweeps=30)
+    o.stop_tol = 1e-13
+    g = api.integrate(spec.problem, spec.phi0, o)
+    c, reps, incs = oracle.integrate(spec.problem, spec.phi0, o)
+    assert np.array_equal(g.final_state, c)
+    assert [s.sweeps for s in g.steps] == [r.sweeps for r in reps]
+    assert all(s.sweeps < 30 for s in g.steps)
+
+
+def test_order_of_accuracy_matches_oracle(gpu, oracle):
+    """Temporal order under dt refinement (refinement.cpp:74-122 procedure on a C1-like problem):
+    GPU slopes equal the oracle's within 0.05 and are ~k+1 for k sweeps."""
+    base = P.config_c1(scale=2)  # N = 128
+    T = 0.02
+    ref_spec = P.config_c1(scale=2)
+    fine = api.IntegrateOptions(scheme=1, dt=T / 256, n_steps=256, M=4, n_sweeps=8)
+    ref = api.integrate(ref_spec.problem, ref_spec.phi0, fine).final_state
+    for k in (1, 2, 3):
+        errs_g, errs_c, dts = [], [], []
+        for nsteps in (8, 16, 32):
+            o = api.IntegrateOptions(scheme=1, dt=T / nsteps, n_steps=nsteps, M=4, n_sweeps=k)
+            g = api.integrate(base.problem, base.phi0, o).final_state
+            c, _, _ = oracle.integrate(base.problem, base.phi0, o)
+            errs_g.append(np.mean(np.abs(g - ref)))
+            errs_c.append(np.mean(np.abs(c - ref)))
+            dts.append(T / nsteps)
+        sg = np.polyfit(np.log(dts), np.log(errs_g), 1)[0]
+        sc = np.polyfit(np.log(dts), np.log(errs_c), 1)[0]
+        assert abs(sg - sc) <= 0.05
+        assert abs(sg - (k + 1)) <= 0.5, (k, sg)
