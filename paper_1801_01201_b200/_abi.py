@@ -11,7 +11,7 @@ MAX_REACTIONS = 64
 OK, E_INVALID_ARGUMENT, E_FACTORIZATION, E_SOLVE, E_NUMERIC, E_CAPABILITY, E_CUDA = range(7)
 PROBLEM_PERIODIC_ADR, PROBLEM_REFERENCE_RD, PROBLEM_LINEAR_SCALAR = 0, 1, 2
 REACTION_NONE, REACTION_LINEAR_DECAY, REACTION_BISTABLE, REACTION_MASS_ACTION = 0, 1, 2, 3
-DIFFUSION_DIRECT, DIFFUSION_MULTIGRID = 0, 1
+DIFFUSION_DIRECT, DIFFUSION_MULTIGRID, DIFFUSION_BANDED_ORACLE = 0, 1, 2
 FIELD_PHI, FIELD_FA, FIELD_FD, FIELD_FR, FIELD_PHI_AD = 0, 1, 2, 3, 4
 STAGE_ADVECTION, STAGE_DIFFUSION, STAGE_REACTION, STAGE_COUPLED = 0, 1, 2, 3
 

@@ -202,12 +202,13 @@ double F8(const cisdc_gpu_ctx* c) { return 8.0 * (double)c->g.n; }  // bytes of 
 // ---------------------------------------------------------------- kernel launchers
 
 int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd, cudaStream_t s) {
-  const int blocks = grid_of(ctx->g.n, 256);
+  const Geom& g = ctx->g;
+  const dim3 grid = stencil_grid(g.nx, g.ny, g.nz, g.S, g.ndim), block = stencil_block(g.ndim);
   ctx->tm.before(kKEvalAD, s);
-  switch (ctx->g.ndim) {
-    case 1: k_eval_ad<1><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
-    case 2: k_eval_ad<2><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
-    default: k_eval_ad<3><<<blocks, 256, 0, s>>>(ctx->ops, ctx->g, phi, fa, fd); break;
+  switch (g.ndim) {
+    case 1: k_eval_ad<1><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
+    case 2: k_eval_ad<2><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
+    default: k_eval_ad<3><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
   }
   ctx->tm.after(kKEvalAD, s, F8(ctx) * (1 + (fa != nullptr) + (fd != nullptr)));
   CU(cudaGetLastError());
@@ -297,11 +298,24 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t 
   }
 }
 
+// compulsory traffic = distinct arrays (right after initialize every node view aliases node 0)
+double distinct_fields(std::vector<const void*> p) {
+  p.erase(std::remove(p.begin(), p.end(), nullptr), p.end());
+  std::sort(p.begin(), p.end());
+  return (double)(std::unique(p.begin(), p.end()) - p.begin());
+}
+
 int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
-  double fields;
-  if (a.kind == kRhsMisdc) fields = 1 + 3.0 * (a.M + 1) + 3 + 2;
-  else if (a.kind == kRhsMisdcq) fields = 1 + 6.0 * a.nt + 1 + 1 + (a.out2 != nullptr);
-  else fields = 1 + 6.0 * a.nt + 3 + 1;
+  std::vector<const void*> in;
+  if (a.kind == kRhsMisdc) {
+    in.push_back(a.phim);
+    for (int j = 0; j <= a.M; ++j) in.insert(in.end(), {a.sfa[j], a.sfd[j], a.sfr[j]});
+  } else {
+    in.push_back(a.base);
+    for (int t = 0; t < a.nt; ++t) in.insert(in.end(), {a.t[t].A, a.t[t].Ap, a.t[t].D, a.t[t].Dp, a.t[t].R, a.t[t].Rp});
+  }
+  in.insert(in.end(), {a.X, a.Y, a.Z});
+  const double fields = distinct_fields(in) + 1 + (a.out2 != nullptr) + (a.base_out != nullptr);
   ctx->tm.before(kKRhs, s);
   k_rhs<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(a, ctx->g.n);
   ctx->tm.after(kKRhs, s, F8(ctx) * fields);
@@ -324,7 +338,9 @@ int launch_quad_base(cisdc_gpu_ctx* ctx, int set, double dt, cudaStream_t s) {
   for (int m = 0; m < M; ++m) q.base[m] = ctx->base[m];
   ctx->tm.before(kKQuad, s);
   k_quad_base<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(q, ctx->g.n);
-  ctx->tm.after(kKQuad, s, F8(ctx) * (1 + 3.0 * (M + 1) + M));
+  std::vector<const void*> in{q.phi0};
+  for (int j = 0; j <= M; ++j) in.insert(in.end(), {q.fa[j], q.fd[j], q.fr[j]});
+  ctx->tm.after(kKQuad, s, F8(ctx) * (distinct_fields(in) + M));
   CU(cudaGetLastError());
   return CISDC_OK;
 }

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "stencil.cuh"
 
 namespace cisdc_b200 {
 
@@ -78,12 +79,7 @@ __device__ __forceinline__ double mg_ax(const MgCoef& C, int s, const double* __
   return __ldg(x + ((long long)k * ny + j) * nx + i) - C.coef * lap;
 }
 
-__device__ __forceinline__ void mg_ijk(long long c, int nx, int ny, int& i, int& j, int& k) {
-  i = static_cast<int>(c % nx);
-  c /= nx;
-  j = static_cast<int>(c % ny);
-  k = static_cast<int>(c / ny);
-}
+// All level kernels run on the 3-D grid of stencil.cuh (x, y, z * S): no integer division per point.
 
 __global__ void k_mg_absmax(const double* __restrict__ b, long long ncell, double* __restrict__ out) {
   const int s = blockIdx.y;
@@ -100,20 +96,18 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_resmax(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                    const double* __restrict__ b, int nx, int ny, int nz,
                                                    const int* __restrict__ active, double* __restrict__ out) {
-  const int s = blockIdx.y;
-  if (!active[s]) return;
+  Pt p;
+  const bool in = grid_point(nx, ny, nz, p);
+  if (!active[p.s]) return;  // uniform per block
   const long long ncell = (long long)nx * ny * nz;
-  const double* xs = x + (long long)s * ncell;
-  const double* bs = b + (long long)s * ncell;
   double m = 0.0;
-  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += (long long)gridDim.x * blockDim.x) {
-    int i, j, k;
-    mg_ijk(c, nx, ny, i, j, k);
-    m = fmax(m, fabs(bs[c] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k)));
+  if (in) {
+    const double* xs = x + (long long)p.s * ncell;
+    m = fabs(b[(long long)p.s * ncell + p.cell] - mg_ax<DIM>(C, p.s, xs, nx, ny, nz, p.i, p.j, p.k));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
-  if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out + s, m);
+  if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0 && m > 0.0) atomic_max_nonneg(out + p.s, m);
 }
 
 // per-species stop decision of the oracle's loop: rn <= tol*bn -> done; cap -> failure
@@ -148,35 +142,32 @@ template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_smooth(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                    const double* __restrict__ b, double* __restrict__ xo, int nx,
                                                    int ny, int nz, int from_zero, const int* __restrict__ active) {
-  const int s = blockIdx.y;
-  if (!active[s]) return;
+  Pt p;
+  if (!grid_point(nx, ny, nz, p)) return;
+  if (!active[p.s]) return;
   const long long ncell = (long long)nx * ny * nz;
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= ncell) return;
-  const long long e = (long long)s * ncell + c;
+  const long long e = (long long)p.s * ncell + p.cell;
   if (from_zero) {
-    xo[e] = C.wD[s] * b[e];
+    xo[e] = C.wD[p.s] * b[e];
     return;
   }
-  int i, j, k;
-  mg_ijk(c, nx, ny, i, j, k);
-  const double* xs = x + (long long)s * ncell;
-  const double r = b[e] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k);
-  xo[e] = xs[c] + C.wD[s] * r;
+  const double* xs = x + (long long)p.s * ncell;
+  const double r = b[e] - mg_ax<DIM>(C, p.s, xs, nx, ny, nz, p.i, p.j, p.k);
+  xo[e] = xs[p.cell] + C.wD[p.s] * r;
 }
 
+// launched on the COARSE grid
 template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_restrict(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                      const double* __restrict__ b, int nx, int ny, int nz,
                                                      double* __restrict__ bc, int cx, int cy, int cz,
                                                      const int* __restrict__ active) {
-  const int s = blockIdx.y;
+  Pt p;
+  if (!grid_point(cx, cy, cz, p)) return;
+  const int s = p.s;
   if (!active[s]) return;
+  const int I = p.i, J = p.j, K = p.k;
   const long long nc = (long long)cx * cy * cz;
-  const long long C0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (C0 >= nc) return;
-  int I, J, K;
-  mg_ijk(C0, cx, cy, I, J, K);
   const long long nf = (long long)nx * ny * nz;
   const double* xs = x + (long long)s * nf;
   const double* bs = b + (long long)s * nf;
@@ -192,20 +183,19 @@ __global__ void __launch_bounds__(256) k_mg_restrict(const __grid_constant__ MgC
         const long long id = ((long long)k * ny + j) * nx + i;
         acc = acc + (bs[id] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k));
       }
-  bc[(long long)s * nc + C0] = acc * scale;
+  bc[(long long)s * nc + p.cell] = acc * scale;
 }
 
 template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_prolong(double* __restrict__ x, int nx, int ny, int nz,
                                                     const double* __restrict__ ec, int cx, int cy, int cz,
                                                     const int* __restrict__ active) {
-  const int s = blockIdx.y;
+  Pt p;
+  if (!grid_point(nx, ny, nz, p)) return;
+  const int s = p.s;
   if (!active[s]) return;
+  const int i = p.i, j = p.j, k = p.k;
   const long long nf = (long long)nx * ny * nz;
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nf) return;
-  int i, j, k;
-  mg_ijk(c, nx, ny, i, j, k);
   const double* e = ec + (long long)s * cx * cy * cz;
   const int I = i >> 1, I2 = wrapi((i & 1) ? I + 1 : I - 1, cx);
   int J = j, J2 = j, K = k, K2 = k;
@@ -235,7 +225,7 @@ __global__ void __launch_bounds__(256) k_mg_prolong(double* __restrict__ x, int 
     v = 0.75 * b0 + 0.25 * b1;
   }
 #undef E_
-  const long long id = (long long)s * nf + c;
+  const long long id = (long long)s * nf + p.cell;
   x[id] = x[id] + v;
 }
 
@@ -339,12 +329,13 @@ struct MgRunner {
   const double* b0;
 
   const double* bof(int l) const { return l == 0 ? b0 : h.lv[l].b; }
-  dim3 grid(long long ncell) const { return dim3((unsigned)((ncell + 255) / 256), (unsigned)h.S, 1); }
+  dim3 grid(const MgLevel& Lv) const { return stencil_grid(Lv.nx, Lv.ny, Lv.nz, h.S, DIM); }
+  dim3 block() const { return stencil_block(DIM); }
 
   void smooth(int l, bool from_zero) {
     MgLevel& Lv = h.lv[l];
     hook->before(kKMgSmooth, s);
-    k_mg_smooth<DIM><<<grid(Lv.ncell), 256, 0, s>>>(C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
+    k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
                                                     h.d_active);
     hook->after(kKMgSmooth, s, 8.0 * Lv.ncell * h.S * (from_zero ? 2 : 3));
     std::swap(Lv.x, Lv.t);
@@ -359,12 +350,12 @@ struct MgRunner {
     for (int it = 0; it < d.mg_pre; ++it) smooth(l, l > 0 && it == 0);
     MgLevel& Cl = h.lv[l + 1];
     hook->before(kKMgRestrict, s);
-    k_mg_restrict<DIM><<<grid(Cl.ncell), 256, 0, s>>>(C[l], Lv.x, bof(l), Lv.nx, Lv.ny, Lv.nz, Cl.b, Cl.nx, Cl.ny,
+    k_mg_restrict<DIM><<<grid(Cl), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.nx, Lv.ny, Lv.nz, Cl.b, Cl.nx, Cl.ny,
                                                       Cl.nz, h.d_active);
     hook->after(kKMgRestrict, s, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell));
     vcycle(l + 1);
     hook->before(kKMgProlong, s);
-    k_mg_prolong<DIM><<<grid(Lv.ncell), 256, 0, s>>>(Lv.x, Lv.nx, Lv.ny, Lv.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
+    k_mg_prolong<DIM><<<grid(Lv), block(), 0, s>>>(Lv.x, Lv.nx, Lv.ny, Lv.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
     hook->after(kKMgProlong, s, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell));
     for (int it = 0; it < d.mg_post; ++it) smooth(l, false);
   }
@@ -402,7 +393,7 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   for (;;) {
     for (int b = 0; b < batch; ++b) {
       hook->before(kKMgNorm, s);
-      k_mg_resmax<DIM><<<rgrid, 256, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
+      k_mg_resmax<DIM><<<R.grid(L0), R.block(), 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
       hook->after(kKMgNorm, s, 16.0 * n);
       hook->before(kKMgNorm, s);
       k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,

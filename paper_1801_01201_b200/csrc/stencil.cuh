@@ -83,24 +83,39 @@ __device__ __forceinline__ double rd_diff(const Ops& o, const double* __restrict
                        16.0 * rd_ext(o, f, n, i + 1) - rd_ext(o, f, n, i + 2));
 }
 
-// element id -> (s, i, j, k)
-__device__ __forceinline__ void decompose(const Geom& g, long long e, int& s, int& i, int& j, int& k) {
-  s = static_cast<int>(e / g.ncell);
-  long long c = e - (long long)s * g.ncell;
-  i = static_cast<int>(c % g.nx);
-  c /= g.nx;
-  j = static_cast<int>(c % g.ny);
-  k = static_cast<int>(c / g.ny);
+// 3-D launch over (x, y, z * S): block (256,1) in 1-D, (32,8) otherwise; the point comes straight
+// from the block/thread indices (no 64-bit integer division per element).
+struct Pt {
+  int i, j, k, s;
+  long long cell;  // index within one species plane
+};
+
+__device__ __forceinline__ bool grid_point(int nx, int ny, int nz, Pt& p) {
+  p.i = blockIdx.x * blockDim.x + threadIdx.x;
+  p.j = blockIdx.y * blockDim.y + threadIdx.y;
+  const unsigned zs = blockIdx.z;
+  p.k = (int)(zs % (unsigned)nz);
+  p.s = (int)(zs / (unsigned)nz);
+  p.cell = ((long long)p.k * ny + p.j) * nx + p.i;
+  return p.i < nx && p.j < ny;
 }
+
+#ifndef __CUDACC_RTC__
+inline dim3 stencil_block(int ndim) { return ndim == 1 ? dim3(256, 1, 1) : dim3(32, 8, 1); }
+inline dim3 stencil_grid(int nx, int ny, int nz, int S, int ndim) {
+  const dim3 b = stencil_block(ndim);
+  return dim3((unsigned)((nx + b.x - 1) / b.x), (unsigned)((ny + b.y - 1) / b.y), (unsigned)(nz * S));
+}
+#endif
 
 // F_A and/or F_D of phi (either output may be null)
 template <int DIM>
 __global__ void __launch_bounds__(256) k_eval_ad(Ops o, Geom g, const double* __restrict__ phi,
                                                  double* __restrict__ fa, double* __restrict__ fd) {
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= g.n) return;
-  int s, i, j, k;
-  decompose(g, e, s, i, j, k);
+  Pt p;
+  if (!grid_point(g.nx, g.ny, g.nz, p)) return;
+  const int s = p.s, i = p.i, j = p.j, k = p.k;
+  const long long e = (long long)s * g.ncell + p.cell;
   const double* f = phi + (long long)s * g.ncell;
   if (o.ref_rd) {
     if (fa) fa[e] = rd_adv(o, f, g.nx, i);
