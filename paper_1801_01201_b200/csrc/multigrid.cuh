@@ -92,22 +92,32 @@ __global__ void k_mg_absmax(const double* __restrict__ b, long long ncell, doubl
   if ((threadIdx.x & 31) == 0) atomic_max_nonneg(out + s, m);
 }
 
+// grid (tiles_x, tiles_y, S); every thread walks its (i, j) column over all k, one atomic per block
 template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_resmax(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                    const double* __restrict__ b, int nx, int ny, int nz,
                                                    const int* __restrict__ active, double* __restrict__ out) {
-  Pt p;
-  const bool in = grid_point(nx, ny, nz, p);
-  if (!active[p.s]) return;  // uniform per block
+  __shared__ double red[8];
+  const int s = blockIdx.z;
+  if (!active[s]) return;  // uniform per block
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
   const long long ncell = (long long)nx * ny * nz;
+  const double* xs = x + (long long)s * ncell;
+  const double* bs = b + (long long)s * ncell;
   double m = 0.0;
-  if (in) {
-    const double* xs = x + (long long)p.s * ncell;
-    m = fabs(b[(long long)p.s * ncell + p.cell] - mg_ax<DIM>(C, p.s, xs, nx, ny, nz, p.i, p.j, p.k));
-  }
+  if (i < nx && j < ny)
+    for (int k = 0; k < nz; ++k)
+      m = fmax(m, fabs(bs[((long long)k * ny + j) * nx + i] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k)));
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
-  if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0 && m > 0.0) atomic_max_nonneg(out + p.s, m);
+  const int t = threadIdx.y * blockDim.x + threadIdx.x;
+  if ((t & 31) == 0) red[t >> 5] = m;
+  __syncthreads();
+  if (t == 0) {
+    for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) m = fmax(m, red[w]);
+    if (m > 0.0) atomic_max_nonneg(out + s, m);
+  }
 }
 
 // per-species stop decision of the oracle's loop: rn <= tol*bn -> done; cap -> failure
@@ -393,7 +403,9 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   for (;;) {
     for (int b = 0; b < batch; ++b) {
       hook->before(kKMgNorm, s);
-      k_mg_resmax<DIM><<<R.grid(L0), R.block(), 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
+      const dim3 rb = R.block();
+      const dim3 rg((L0.nx + rb.x - 1) / rb.x, (L0.ny + rb.y - 1) / rb.y, g.S);
+      k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
       hook->after(kKMgNorm, s, 16.0 * n);
       hook->before(kKMgNorm, s);
       k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
