@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "stencil.cuh"
+#include "stencil3d.cuh"
 
 namespace cisdc_b200 {
 
@@ -164,6 +165,78 @@ __global__ void __launch_bounds__(256) k_mg_smooth(const __grid_constant__ MgCoe
   const double* xs = x + (long long)p.s * ncell;
   const double r = b[e] - mg_ax<DIM>(C, p.s, xs, nx, ny, nz, p.i, p.j, p.k);
   xo[e] = xs[p.cell] + C.wD[p.s] * r;
+}
+
+// 3-D levels: 2.5-D blocked versions (stencil3d.cuh) of the smoother and the residual norm.
+// A x at (i,j,k) from the tile / z-queue taps, same expression as mg_ax.
+__device__ __forceinline__ double mg_ax_taps(const MgCoef& C, int s, const double (&v)[3][5]) {
+  double lap = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+    lap = lap + C.c[s][a] * (-v[a][0] + 16.0 * v[a][1] - 30.0 * v[a][2] + 16.0 * v[a][3] - v[a][4]);
+  return v[0][2] - C.coef * lap;
+}
+
+// mode 0: smooth x -> xo (not from zero); mode 1: residual inf-norm into out[s]
+template <int MODE>
+__global__ void __launch_bounds__(kTX* kTY) k_mg3_tiled(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+                                                         const double* __restrict__ b, double* __restrict__ xo,
+                                                         int nx, int ny, int nz, int kc, const int* __restrict__ active,
+                                                         double* __restrict__ out) {
+  __shared__ double tile[kTileH][kTileW + 1];
+  __shared__ double red[kTX * kTY / 32];
+  const ZChunk z = zchunk(nz, kc);
+  if (!active[z.s]) return;  // uniform per block
+  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
+  const int i = i0 + threadIdx.x, j = j0 + threadIdx.y;
+  const bool in = i < nx && j < ny;
+  const long long ncell = (long long)nx * ny * nz, pl = (long long)nx * ny;
+  const long long col = (long long)(in ? j : 0) * nx + (in ? i : 0);
+  const double* f = x + (long long)z.s * ncell;
+  double q0 = __ldg(f + wrapi(z.k0 - 2, nz) * pl + col);
+  double q1 = __ldg(f + wrapi(z.k0 - 1, nz) * pl + col);
+  double q2 = __ldg(f + (long long)z.k0 * pl + col);
+  double q3 = __ldg(f + wrapi(z.k0 + 1, nz) * pl + col);
+  const int tx = threadIdx.x + kHalo, ty = threadIdx.y + kHalo;
+  double m = 0.0;
+  for (int k = z.k0; k < z.k1; ++k) {
+    const double q4 = __ldg(f + wrapi(k + 2, nz) * pl + col);
+    __syncthreads();
+    load_tile(tile, f, nx, ny, i0, j0, k);
+    __syncthreads();
+    if (in) {
+      double v[3][5];
+#pragma unroll
+      for (int o2 = 0; o2 < 5; ++o2) {
+        v[0][o2] = tile[ty][tx + o2 - 2];
+        v[1][o2] = tile[ty + o2 - 2][tx];
+      }
+      v[2][0] = q0;
+      v[2][1] = q1;
+      v[2][2] = q2;
+      v[2][3] = q3;
+      v[2][4] = q4;
+      const long long e = (long long)z.s * ncell + (long long)k * pl + col;
+      const double r = b[e] - mg_ax_taps(C, z.s, v);
+      if (MODE == 0) xo[e] = q2 + C.wD[z.s] * r;
+      else m = fmax(m, fabs(r));
+    }
+    q0 = q1;
+    q1 = q2;
+    q2 = q3;
+    q3 = q4;
+  }
+  if (MODE == 1) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+    const int t = threadIdx.y * kTX + threadIdx.x;
+    if ((t & 31) == 0) red[t >> 5] = m;
+    __syncthreads();
+    if (t == 0) {
+      for (int w = 1; w < kTX * kTY / 32; ++w) m = fmax(m, red[w]);
+      if (m > 0.0) atomic_max_nonneg(out + z.s, m);
+    }
+  }
 }
 
 // launched on the COARSE grid
@@ -345,7 +418,11 @@ struct MgRunner {
   void smooth(int l, bool from_zero) {
     MgLevel& Lv = h.lv[l];
     hook->before(kKMgSmooth, s);
-    k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
+    if (DIM == 3 && !from_zero)
+      k_mg3_tiled<0><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
+          C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, nullptr);
+    else
+      k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
                                                     h.d_active);
     hook->after(kKMgSmooth, s, 8.0 * Lv.ncell * h.S * (from_zero ? 2 : 3));
     std::swap(Lv.x, Lv.t);
@@ -405,7 +482,11 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
       hook->before(kKMgNorm, s);
       const dim3 rb = R.block();
       const dim3 rg((L0.nx + rb.x - 1) / rb.x, (L0.ny + rb.y - 1) / rb.y, g.S);
-      k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
+      if (DIM == 3)
+        k_mg3_tiled<1><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
+            R.C[0], L0.x, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax);
+      else
+        k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
       hook->after(kKMgNorm, s, 16.0 * n);
       hook->before(kKMgNorm, s);
       k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
