@@ -377,6 +377,10 @@ static int newton_scalar_cell(const co_problem* p, double coef, double b, double
 
 /* vector Newton: newton_scalar's control flow with inf-norms, Jacobian solve by
    lu_factor_dense(pivoting=true) + lu_solve; a pivot below 1e-300 is a singular Jacobian */
+/* diagnostic: row interchanges performed by the vector Newton's LU (process-wide) */
+long long co_pivot_swaps = 0;
+long long co_get_pivot_swaps(void) { return co_pivot_swaps; }
+
 static int newton_vector_cell(const co_problem* p, double coef, const double* b, double* x, long long* trips) {
   const int S = p->S;
   const double tol = p->d.newton_tol;
@@ -406,6 +410,7 @@ static int newton_vector_cell(const co_problem* p, double coef, const double* b,
           pv = i;
         }
       if (pv != kk) {
+        ++co_pivot_swaps;
         for (int j = 0; j < S; ++j) {
           const double t = J[kk * S + j];
           J[kk * S + j] = J[pv * S + j];

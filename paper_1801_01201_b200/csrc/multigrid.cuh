@@ -187,45 +187,17 @@ __global__ void __launch_bounds__(kTX* kTY) k_mg3_tiled(const __grid_constant__ 
   __shared__ double red[kTX * kTY / 32];
   const ZChunk z = zchunk(nz, kc);
   if (!active[z.s]) return;  // uniform per block
-  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
-  const int i = i0 + threadIdx.x, j = j0 + threadIdx.y;
-  const bool in = i < nx && j < ny;
-  const long long ncell = (long long)nx * ny * nz, pl = (long long)nx * ny;
-  const long long col = (long long)(in ? j : 0) * nx + (in ? i : 0);
-  const double* f = x + (long long)z.s * ncell;
-  double q0 = __ldg(f + wrapi(z.k0 - 2, nz) * pl + col);
-  double q1 = __ldg(f + wrapi(z.k0 - 1, nz) * pl + col);
-  double q2 = __ldg(f + (long long)z.k0 * pl + col);
-  double q3 = __ldg(f + wrapi(z.k0 + 1, nz) * pl + col);
-  const int tx = threadIdx.x + kHalo, ty = threadIdx.y + kHalo;
+  const long long ncell = (long long)nx * ny * nz;
+  const long long sbase = (long long)z.s * ncell;
+  const double* f = x + sbase;
+  const int s = z.s;
   double m = 0.0;
-  for (int k = z.k0; k < z.k1; ++k) {
-    const double q4 = __ldg(f + wrapi(k + 2, nz) * pl + col);
-    __syncthreads();
-    load_tile(tile, f, nx, ny, i0, j0, k);
-    __syncthreads();
-    if (in) {
-      double v[3][5];
-#pragma unroll
-      for (int o2 = 0; o2 < 5; ++o2) {
-        v[0][o2] = tile[ty][tx + o2 - 2];
-        v[1][o2] = tile[ty + o2 - 2][tx];
-      }
-      v[2][0] = q0;
-      v[2][1] = q1;
-      v[2][2] = q2;
-      v[2][3] = q3;
-      v[2][4] = q4;
-      const long long e = (long long)z.s * ncell + (long long)k * pl + col;
-      const double r = b[e] - mg_ax_taps(C, z.s, v);
-      if (MODE == 0) xo[e] = q2 + C.wD[z.s] * r;
-      else m = fmax(m, fabs(r));
-    }
-    q0 = q1;
-    q1 = q2;
-    q2 = q3;
-    q3 = q4;
-  }
+  walk_tiled(f, nx, ny, nz, z, tile, [&](int, long long cell, int, int, const double (&v)[3][5]) {
+    const long long e = sbase + cell;
+    const double r = b[e] - mg_ax_taps(C, s, v);
+    if (MODE == 0) xo[e] = v[2][2] + C.wD[s] * r;
+    else m = fmax(m, fabs(r));
+  });
   if (MODE == 1) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));

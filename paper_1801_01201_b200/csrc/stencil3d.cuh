@@ -3,10 +3,12 @@
 //
 // A (32, 8) thread block owns an x-y tile and walks a chunk of z-planes.  Each thread keeps its
 // column's five z-values (k-2 .. k+2) in a register queue; the x/y neighbours of plane k come from a
-// shared-memory tile with a 2-cell periodic halo.  Every input value is fetched from HBM once per
-// chunk (plus the tile halo, from L2), instead of once per stencil tap.  The arithmetic is the
-// generic kernels' expressions with the same operand order (same bits): only the data source of
-// each tap changes.
+// shared-memory tile with a 2-cell periodic halo.  The next plane's tile is prefetched into
+// registers while the current plane is computed (its L2 latency overlaps the arithmetic), and the
+// periodic tile offsets are computed once per block, not per plane.  Every input value is fetched
+// from HBM once per chunk (plus the tile halo, from L2) instead of once per stencil tap.  The
+// arithmetic is the generic kernels' expressions in the same operand order (same bits): only the
+// data source of each tap changes.
 #pragma once
 
 #include "common.cuh"
@@ -16,23 +18,43 @@ namespace cisdc_b200 {
 
 constexpr int kTX = 32, kTY = 8, kHalo = 2;
 constexpr int kTileW = kTX + 2 * kHalo, kTileH = kTY + 2 * kHalo;
+constexpr int kTileN = kTileW * kTileH;                         // 432
+constexpr int kTilePer = (kTileN + kTX * kTY - 1) / (kTX * kTY);  // 2 elements per thread
 
 __device__ __forceinline__ int wrap_any(int x, int n) {
   x %= n;
   return x < 0 ? x + n : x;
 }
 
-// tile[r][c] = f(i0 + c - 2, j0 + r - 2, k) periodic; called by all threads of the block
-__device__ __forceinline__ void load_tile(double (*tile)[kTileW + 1], const double* __restrict__ f, int nx, int ny,
-                                          int i0, int j0, int k) {
-  const int t = threadIdx.y * kTX + threadIdx.x;
-  const long long plane = (long long)k * ny * nx;
-  for (int idx = t; idx < kTileW * kTileH; idx += kTX * kTY) {
-    const int r = idx / kTileW, c = idx - r * kTileW;
-    const int gi = wrap_any(i0 + c - kHalo, nx), gj = wrap_any(j0 + r - kHalo, ny);
-    tile[r][c] = __ldg(f + plane + (long long)gj * nx + gi);
+// The (up to) two tile elements this thread stages: smem slot and in-plane global offset.
+struct TileLoader {
+  int slot[kTilePer];
+  long long off[kTilePer];
+  __device__ __forceinline__ void init(int nx, int ny, int i0, int j0) {
+    const int t = threadIdx.y * kTX + threadIdx.x;
+#pragma unroll
+    for (int u = 0; u < kTilePer; ++u) {
+      const int idx = t + u * kTX * kTY;
+      if (idx < kTileN) {
+        const int r = idx / kTileW, c = idx - r * kTileW;
+        slot[u] = r * (kTileW + 1) + c;
+        off[u] = (long long)wrap_any(j0 + r - kHalo, ny) * nx + wrap_any(i0 + c - kHalo, nx);
+      } else {
+        slot[u] = -1;
+        off[u] = 0;
+      }
+    }
   }
-}
+  __device__ __forceinline__ void fetch(const double* __restrict__ plane, double (&v)[kTilePer]) const {
+#pragma unroll
+    for (int u = 0; u < kTilePer; ++u) v[u] = slot[u] >= 0 ? __ldg(plane + off[u]) : 0.0;
+  }
+  __device__ __forceinline__ void store(double* tile, const double (&v)[kTilePer]) const {
+#pragma unroll
+    for (int u = 0; u < kTilePer; ++u)
+      if (slot[u] >= 0) tile[slot[u]] = v[u];
+  }
+};
 
 // z-chunking: blockIdx.z = s * nzc + zc
 struct ZChunk {
@@ -56,29 +78,30 @@ inline dim3 tile3d_grid(int nx, int ny, int nz, int S) {
 }
 #endif
 
-// F_A and/or F_D, 3-D periodic
-__global__ void __launch_bounds__(kTX* kTY) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
-                                                              double* __restrict__ fa, double* __restrict__ fd,
-                                                              int kc) {
-  __shared__ double tile[kTileH][kTileW + 1];
-  const ZChunk z = zchunk(g.nz, kc);
+// Walks the z-chunk of one species stack f, calling body(k, v) for every in-range point with the
+// 3 x 5 taps v[axis][offset + 2] of plane k.
+template <class Body>
+__device__ __forceinline__ void walk_tiled(const double* __restrict__ f, int nx, int ny, int nz, const ZChunk& z,
+                                           double (*tile)[kTileW + 1], Body body) {
   const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
   const int i = i0 + threadIdx.x, j = j0 + threadIdx.y;
-  const bool in = i < g.nx && j < g.ny;
-  const int ic = in ? i : 0, jc = in ? j : 0;
-  const double* f = phi + (long long)z.s * g.ncell;
-  const long long col = (long long)jc * g.nx + ic, pl = (long long)g.nx * g.ny;
-  double q0 = __ldg(f + wrapi(z.k0 - 2, g.nz) * pl + col);
-  double q1 = __ldg(f + wrapi(z.k0 - 1, g.nz) * pl + col);
+  const bool in = i < nx && j < ny;
+  const long long pl = (long long)nx * ny;
+  const long long col = (long long)(in ? j : 0) * nx + (in ? i : 0);
+  TileLoader L;
+  L.init(nx, ny, i0, j0);
+  double pre[kTilePer];
+  L.fetch(f + (long long)z.k0 * pl, pre);
+  double q0 = __ldg(f + wrapi(z.k0 - 2, nz) * pl + col);
+  double q1 = __ldg(f + wrapi(z.k0 - 1, nz) * pl + col);
   double q2 = __ldg(f + (long long)z.k0 * pl + col);
-  double q3 = __ldg(f + wrapi(z.k0 + 1, g.nz) * pl + col);
+  double q3 = __ldg(f + wrapi(z.k0 + 1, nz) * pl + col);
+  L.store(&tile[0][0], pre);
   const int tx = threadIdx.x + kHalo, ty = threadIdx.y + kHalo;
-  const int im1 = wrapi(i - 1, g.nx), jm1 = wrapi(j - 1, g.ny);
   for (int k = z.k0; k < z.k1; ++k) {
-    const double q4 = __ldg(f + wrapi(k + 2, g.nz) * pl + col);
-    __syncthreads();
-    load_tile(tile, f, g.nx, g.ny, i0, j0, k);
-    __syncthreads();
+    __syncthreads();  // tile(k) complete
+    const double q4 = __ldg(f + wrapi(k + 2, nz) * pl + col);
+    if (k + 1 < z.k1) L.fetch(f + (long long)(k + 1) * pl, pre);
     if (in) {
       double v[3][5];
 #pragma unroll
@@ -91,32 +114,48 @@ __global__ void __launch_bounds__(kTX* kTY) k_eval_ad3_tiled(Ops o, Geom g, cons
       v[2][2] = q2;
       v[2][3] = q3;
       v[2][4] = q4;
-      const long long e = (long long)z.s * g.ncell + (long long)k * pl + col;
-      if (fa) {
-        double acc = 0.0;
-        const int km1 = wrapi(k - 1, g.nz);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          if (!o.adv[a]) continue;
-          const int ia = a == 0 ? im1 : i, ja = a == 1 ? jm1 : j, ka = a == 2 ? km1 : k;
-          const double fr = face_u(o, a, i, j, k) * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
-          const double fl = face_u(o, a, ia, ja, ka) * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
-          acc = acc + (fr - fl) * o.cadv[a];
-        }
-        fa[e] = -acc;
-      }
-      if (fd) {
-        double lap = 0.0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) lap = lap + o.cdiff[z.s][a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
-        fd[e] = lap;
-      }
+      body(k, (long long)k * pl + col, i, j, v);
     }
+    __syncthreads();  // everyone is done with tile(k)
+    if (k + 1 < z.k1) L.store(&tile[0][0], pre);
     q0 = q1;
     q1 = q2;
     q2 = q3;
     q3 = q4;
   }
+}
+
+// F_A and/or F_D, 3-D periodic
+__global__ void __launch_bounds__(kTX* kTY) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
+                                                              double* __restrict__ fa, double* __restrict__ fd,
+                                                              int kc) {
+  __shared__ double tile[kTileH][kTileW + 1];
+  const ZChunk z = zchunk(g.nz, kc);
+  const double* f = phi + (long long)z.s * g.ncell;
+  const long long sbase = (long long)z.s * g.ncell;
+  const int s = z.s;
+  walk_tiled(f, g.nx, g.ny, g.nz, z, tile, [&](int k, long long cell, int i, int j, const double (&v)[3][5]) {
+    const long long e = sbase + cell;
+    if (fa) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        if (!o.adv[a]) continue;
+        const int ia = a == 0 ? wrapi(i - 1, g.nx) : i, ja = a == 1 ? wrapi(j - 1, g.ny) : j,
+                  ka = a == 2 ? wrapi(k - 1, g.nz) : k;
+        const double fr = face_u(o, a, i, j, k) * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
+        const double fl = face_u(o, a, ia, ja, ka) * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
+        acc = acc + (fr - fl) * o.cadv[a];
+      }
+      fa[e] = -acc;
+    }
+    if (fd) {
+      double lap = 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) lap = lap + o.cdiff[s][a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
+      fd[e] = lap;
+    }
+  });
 }
 
 }  // namespace cisdc_b200
