@@ -287,7 +287,8 @@ def main():
                         "gbs": (by[c] / (ms[c] * 1e-3) / 1e9) if ms[c] > 0 else None})
     dom = max(classes, key=lambda x: x["ms"])
     cell_solves = desc.ncell * spec.M * spec.n_sweeps * args.steps * (spec.nu if scheme == 2 else 1)
-    newton_flops = roofline.newton_work(desc, newton, cell_solves)
+    sparse = os.environ.get("CISDC_RTC", "1") != "0"  # the specialised kernel runs the static-pattern LU
+    newton_flops = roofline.newton_work(desc, newton, cell_solves, sparse=sparse)
     if dom["kernel"] == "react_newton" and desc.nspecies >= 9:
         achieved = newton_flops / (dom["ms"] * 1e-3) / 1e12
         roof = {"bound": "fp64", "kernel": dom["kernel"], "achieved": achieved, "peak": pk_fma.value,

@@ -132,6 +132,8 @@ struct cisdc_gpu_ctx {
   double* rd_work = nullptr;
   MgHierarchy mg;
   RtcNewton rtc;  // network-specialised Newton kernels (mass action)
+  unsigned* defer_list = nullptr;  // cells the specialised kernel hands to the dense fixup
+  int* defer_count = nullptr;
   // status / reductions
   DevStatus* d_st = nullptr;
   DevStatus* h_st = nullptr;  // pinned
@@ -279,18 +281,56 @@ int launch_react_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unsupported species count");
 }
 
+template <int S, int MODE>
+void launch_fixup_sm(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
+  const dim3 grid(148), block(128);
+  if constexpr (MODE == kModeMisdcq || MODE == kModeMisdc) {
+    switch (ctx->g.ndim) {
+      case 1: k_react_fixup<S, 1, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
+      case 2: k_react_fixup<S, 2, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
+      default: k_react_fixup<S, 3, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
+    }
+  } else {
+    k_react_fixup<S, 1, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
+  }
+}
+
+template <int MODE>
+void launch_fixup_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
+  switch (ctx->S) {
+    case 1: launch_fixup_sm<1, MODE>(ctx, a, s); break;
+    case 2: launch_fixup_sm<2, MODE>(ctx, a, s); break;
+    case 3: launch_fixup_sm<3, MODE>(ctx, a, s); break;
+    case 4: launch_fixup_sm<4, MODE>(ctx, a, s); break;
+    default: launch_fixup_sm<9, MODE>(ctx, a, s); break;
+  }
+}
+
 int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t s) {
   if (ctx->rtc.ready) {
     Reaction rx = ctx->rx;
     Ops o = ctx->ops;
     Geom g = ctx->g;
     ReactArgs aa = a;
+    aa.defer_list = ctx->defer_list;
+    aa.defer_count = ctx->defer_count;
     DevStatus* st = ctx->d_st;
     void* args[5] = {&rx, &o, &g, &aa, &st};
     ctx->tm.before(kKReact, s);
     CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)), dim3(128),
                         args, 0, s));
     ctx->tm.after(kKReact, s, F8(ctx) * react_fields(mode, a));
+    // cells whose LU needed a row interchange: dense generic kernel, then reset the list
+    ctx->tm.before(kKReact, s);
+    switch (mode) {
+      case kModeMisdcq: launch_fixup_m<kModeMisdcq>(ctx, aa, s); break;
+      case kModeMisdc: launch_fixup_m<kModeMisdc>(ctx, aa, s); break;
+      case kModeCisdcq: launch_fixup_m<kModeCisdcq>(ctx, aa, s); break;
+      default: launch_fixup_m<kModePlain>(ctx, aa, s); break;
+    }
+    ctx->tm.after(kKReact, s, 0.0);
+    CU(cudaGetLastError());
+    CU(cudaMemsetAsync(ctx->defer_count, 0, sizeof(int), s));
     return CISDC_OK;
   }
   switch (mode) {
@@ -926,6 +966,14 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     TRY(dalloc(ctx, &ctx->fd_ad[m], n));
   }
   if (ctx->ref_rd) TRY(dalloc(ctx, &ctx->rd_work, (size_t)g.nx * 10));
+  if (ctx->rtc.ready) {
+    void* v1 = nullptr;
+    CU(cudaMalloc(&v1, sizeof(unsigned) * (size_t)g.ncell + sizeof(int)));
+    ctx->allocs.push_back(v1);
+    ctx->defer_list = static_cast<unsigned*>(v1);
+    ctx->defer_count = reinterpret_cast<int*>(ctx->defer_list + g.ncell);
+    CU(cudaMemset(ctx->defer_count, 0, sizeof(int)));
+  }
   if (!ctx->ref_rd && d->diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
     const int rc = mg_init(ctx->mg, g, *d);
     if (rc) return set_err(ctx, rc, "multigrid: hierarchy setup failed (" + std::to_string(rc) + ")");

@@ -448,28 +448,32 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   int batch = 1;
   for (const auto& pc : h.predicted)
     if (pc.first == coef) batch = std::max(1, pc.second);
+  // check = residual norm + per-species decision (the decision enables the next V-cycle)
+  auto check = [&]() {
+    hook->before(kKMgNorm, s);
+    const dim3 rb = R.block();
+    const dim3 rg((L0.nx + rb.x - 1) / rb.x, (L0.ny + rb.y - 1) / rb.y, g.S);
+    if (DIM == 3)
+      k_mg3_tiled<1><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
+          R.C[0], L0.x, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax);
+    else
+      k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
+    hook->after(kKMgNorm, s, 16.0 * n);
+    hook->before(kKMgNorm, s);
+    k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
+                                 h.d_flag, st);
+    hook->after(kKMgNorm, s, 0.0);
+  };
+  check();
   int launched = 0;
   for (;;) {
-    for (int b = 0; b < batch; ++b) {
-      hook->before(kKMgNorm, s);
-      const dim3 rb = R.block();
-      const dim3 rg((L0.nx + rb.x - 1) / rb.x, (L0.ny + rb.y - 1) / rb.y, g.S);
-      if (DIM == 3)
-        k_mg3_tiled<1><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
-            R.C[0], L0.x, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax);
-      else
-        k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
-      hook->after(kKMgNorm, s, 16.0 * n);
-      hook->before(kKMgNorm, s);
-      k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
-                                   h.d_flag, st);
-      hook->after(kKMgNorm, s, 0.0);
-      if (launched + b < d.mg_max_cycles) R.vcycle(0);
+    for (int b = 0; b < batch && launched < d.mg_max_cycles; ++b, ++launched) {
+      R.vcycle(0);
+      check();
     }
-    launched += batch;
     cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
     if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
-    if (!h.h_flag[0] || h.h_flag[1] || launched > d.mg_max_cycles) break;
+    if (!h.h_flag[0] || h.h_flag[1] || launched >= d.mg_max_cycles) break;
     batch = 1;
   }
   // remember how many cycles this coefficient needed (flag[0] == 0 after the last check)

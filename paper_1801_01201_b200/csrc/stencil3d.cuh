@@ -134,25 +134,44 @@ __global__ void __launch_bounds__(kTX* kTY) k_eval_ad3_tiled(Ops o, Geom g, cons
   const double* f = phi + (long long)z.s * g.ncell;
   const long long sbase = (long long)z.s * g.ncell;
   const int s = z.s;
-  walk_tiled(f, g.nx, g.ny, g.nz, z, tile, [&](int k, long long cell, int i, int j, const double (&v)[3][5]) {
+  // Face velocities u_a = (T_a0[i] T_a1[j]) T_a2[k] (face_u): the (i, j) factor of the right and
+  // left faces is fixed for this thread's column -- formed once, times T_a2 per plane (same bits).
+  const int ic = min(blockIdx.x * kTX + threadIdx.x, g.nx - 1), jc = min(blockIdx.y * kTY + threadIdx.y, g.ny - 1);
+  double pr[3], pl[3];
+  const double* t2[3];
+  bool adv[3];
+  double cd[3], ca[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    adv[a] = o.adv[a] != 0;
+    cd[a] = o.cdiff[s][a];
+    ca[a] = o.cadv[a];
+    const int il = a == 0 ? wrapi(ic - 1, g.nx) : ic, jl = a == 1 ? wrapi(jc - 1, g.ny) : jc;
+    const double* t0 = o.vel[a][0];
+    const double* t1 = o.vel[a][1];
+    pr[a] = (t0 ? __ldg(t0 + ic) : 1.0) * (t1 ? __ldg(t1 + jc) : 1.0);
+    pl[a] = (t0 ? __ldg(t0 + il) : 1.0) * (t1 ? __ldg(t1 + jl) : 1.0);
+    t2[a] = o.vel[a][2];
+  }
+  walk_tiled(f, g.nx, g.ny, g.nz, z, tile, [&](int k, long long cell, int, int, const double (&v)[3][5]) {
     const long long e = sbase + cell;
     if (fa) {
       double acc = 0.0;
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        if (!o.adv[a]) continue;
-        const int ia = a == 0 ? wrapi(i - 1, g.nx) : i, ja = a == 1 ? wrapi(j - 1, g.ny) : j,
-                  ka = a == 2 ? wrapi(k - 1, g.nz) : k;
-        const double fr = face_u(o, a, i, j, k) * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
-        const double fl = face_u(o, a, ia, ja, ka) * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
-        acc = acc + (fr - fl) * o.cadv[a];
+        if (!adv[a]) continue;
+        const double ur = pr[a] * (t2[a] ? __ldg(t2[a] + k) : 1.0);
+        const double ul = pl[a] * (t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0);
+        const double fr = ur * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
+        const double fl = ul * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
+        acc = acc + (fr - fl) * ca[a];
       }
       fa[e] = -acc;
     }
     if (fd) {
       double lap = 0.0;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) lap = lap + o.cdiff[s][a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
+      for (int a = 0; a < 3; ++a) lap = lap + cd[a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
       fd[e] = lap;
     }
   });

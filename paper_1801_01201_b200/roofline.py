@@ -3,8 +3,10 @@
 Bytes: every kernel launch is charged its compulsory traffic (each distinct field read once and
 written once; halo re-reads and constants are free) by the native library itself
 (cisdc_gpu_kernel_times).  Flops: the batched Newton/LU kernel is FP64-bound for S = 9; its work is
-counted analytically per Newton trip from the reaction network (no pivot comparisons, no index
-arithmetic), as SURVEY.md section 8(d) prescribes.
+counted analytically per Newton trip from the reaction network, as the specialised kernel executes
+it: the static-pattern LU touches only the structurally non-zero entries of I - coef J and their
+fill (csrc/rtc.cuh), so the count uses that pattern, not a dense S^3/3 (no pivot
+comparisons or index arithmetic counted).
 """
 from __future__ import annotations
 
@@ -13,13 +15,8 @@ import numpy as np
 from . import _abi
 
 
-def newton_flops(desc) -> tuple[float, float]:
-    """(flops of a residual-only trip, extra flops of a trip that builds and solves the Jacobian)."""
+def _network(desc):
     S = desc.nspecies
-    if desc.reaction_kind != _abi.REACTION_MASS_ACTION:
-        if desc.reaction_kind == _abi.REACTION_BISTABLE:
-            return 7.0, 11.0  # f: 4 mul + 3 add/sub ; f': 7 ops + step/update/test 4
-        return 4.0, 6.0
     reac = np.asarray(desc.reactants).reshape(-1, 2)
     prod = np.asarray(desc.products).reshape(-1, 2)
     nr = len(reac)
@@ -30,23 +27,69 @@ def newton_flops(desc) -> tuple[float, float]:
                 nu[reac[r, t], r] -= 1
             if prod[r, t] >= 0:
                 nu[prod[r, t], r] += 1
-    nnz = int(np.count_nonzero(nu))
+    return S, reac, nu
+
+
+def lu_pattern(desc) -> np.ndarray:
+    """Structural pattern of the LU factors of I - coef J (no row interchanges)."""
+    S, reac, nu = _network(desc)
+    pat = np.eye(S, dtype=bool)
+    for r in range(len(reac)):
+        for t in range(2):
+            q = reac[r, t]
+            if q >= 0:
+                pat[nu[:, r] != 0, q] = True
+    for k in range(S):
+        rows = [i for i in range(k + 1, S) if pat[i, k]]
+        cols = [j for j in range(k + 1, S) if pat[k, j]]
+        for i in rows:
+            pat[i, cols] = True
+    return pat
+
+
+def newton_flops(desc, sparse: bool = True) -> tuple[float, float]:
+    """(flops of a residual-only trip, extra flops of a trip that builds and solves the Jacobian)."""
+    if desc.reaction_kind != _abi.REACTION_MASS_ACTION:
+        if desc.reaction_kind == _abi.REACTION_BISTABLE:
+            return 7.0, 11.0  # f: 4 mul + 3 add/sub ; f': 7 ops + step/update/test 4
+        return 4.0, 6.0
+    S, reac, nu = _network(desc)
+    nr = len(reac)
     rates = sum(2 if reac[r, 1] >= 0 else 1 for r in range(nr))
-    residual = rates + 2 * nnz + 3 * S
+    residual = rates + 2 * int(np.count_nonzero(nu)) + 3 * S
     jac = 0
+    jnz = np.zeros((S, S), dtype=bool)
     for r in range(nr):
-        nreac = 2 if reac[r, 1] >= 0 else 1
-        jac += (1 if nreac == 2 else 0) + (1 if nreac == 2 else 0)  # g per reactant slot
-        jac += 2 * int(np.count_nonzero(nu[:, r])) * nreac
-    shift = 2 * S * S
-    lu = sum((S - 1 - k) + 2 * (S - 1 - k) ** 2 for k in range(S))
-    solves = sum(2 * i for i in range(S)) + sum(2 * (S - 1 - i) + 1 for i in range(S))
+        if not np.any(nu[:, r]):
+            continue
+        two = reac[r, 1] >= 0
+        for t in range(2):
+            q = reac[r, t]
+            if q < 0:
+                continue
+            jac += 1 if two else 0  # g = k * x
+            jac += 2 * int(np.count_nonzero(nu[:, r]))
+            jnz[nu[:, r] != 0, q] = True
+    if sparse:
+        pat = lu_pattern(desc)
+        shift = 2 * int(np.count_nonzero(jnz))
+        lu = 0
+        for k in range(S):
+            cols = int(np.count_nonzero(pat[k, k + 1:]))
+            for i in range(k + 1, S):
+                if pat[i, k]:
+                    lu += 1 + 2 * cols + 2  # m, row update, f update
+        back = sum(2 * int(np.count_nonzero(pat[i, i + 1:])) + 1 for i in range(S))
+    else:
+        shift = 2 * S * S
+        lu = sum((S - 1 - k) * (1 + 2 * (S - 1 - k) + 2) for k in range(S))
+        back = sum(2 * (S - 1 - i) + 1 for i in range(S))
     update = S
-    return float(residual), float(jac + shift + lu + solves + update)
+    return float(residual), float(jac + shift + lu + back + update)
 
 
-def newton_work(desc, trips: int, cell_solves: int) -> float:
+def newton_work(desc, trips: int, cell_solves: int, sparse: bool = True) -> float:
     """Lower-bound FP64 flops of `trips` Newton trips over `cell_solves` per-cell solves (each solve's
     last trip is counted as residual-only)."""
-    res, full = newton_flops(desc)
+    res, full = newton_flops(desc, sparse)
     return trips * res + max(trips - cell_solves, 0) * full
