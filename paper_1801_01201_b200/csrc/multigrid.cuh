@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kTX* kTY) k_mg3_tiled(const __grid_constant__ 
                                                          const double* __restrict__ b, double* __restrict__ xo,
                                                          int nx, int ny, int nz, int kc, const int* __restrict__ active,
                                                          double* __restrict__ out) {
-  __shared__ double tile[kTileH][kTileW + 1];
+  __shared__ TileArr tile;
   __shared__ double red[kTX * kTY / 32];
   const ZChunk z = zchunk(nz, kc);
   if (!active[z.s]) return;  // uniform per block
@@ -191,11 +191,16 @@ __global__ void __launch_bounds__(kTX* kTY) k_mg3_tiled(const __grid_constant__ 
   const long long sbase = (long long)z.s * ncell;
   const double* f = x + sbase;
   const int s = z.s;
+  const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0;
-  walk_tiled(f, nx, ny, nz, z, tile, [&](int, long long cell, int, int, const double (&v)[3][5]) {
-    const long long e = sbase + cell;
-    const double r = b[e] - mg_ax_taps(C, s, v);
-    if (MODE == 0) xo[e] = v[2][2] + C.wD[s] * r;
+  walk_tiled(f, b + sbase, nx, ny, nz, z, tile, [&](int, int, long long cell, const double (&v)[3][5], double bv) {
+    // mg_ax_taps with the species coefficients hoisted (same expression)
+    double lap = 0.0;
+    lap = lap + cs0 * (-v[0][0] + 16.0 * v[0][1] - 30.0 * v[0][2] + 16.0 * v[0][3] - v[0][4]);
+    lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
+    lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
+    const double r = bv - (v[0][2] - coef * lap);
+    if (MODE == 0) xo[sbase + cell] = v[2][2] + wd * r;
     else m = fmax(m, fabs(r));
   });
   if (MODE == 1) {

@@ -1,14 +1,15 @@
 // 2.5-D blocked radius-2 star stencils for 3-D grids (K1 F_A/F_D, and the multigrid smoother /
 // residual of K3).
 //
-// A (32, 8) thread block owns an x-y tile and walks a chunk of z-planes.  Each thread keeps its
-// column's five z-values (k-2 .. k+2) in a register queue; the x/y neighbours of plane k come from a
-// shared-memory tile with a 2-cell periodic halo.  The next plane's tile is prefetched into
-// registers while the current plane is computed (its L2 latency overlaps the arithmetic), and the
-// periodic tile offsets are computed once per block, not per plane.  Every input value is fetched
-// from HBM once per chunk (plus the tile halo, from L2) instead of once per stencil tap.  The
-// arithmetic is the generic kernels' expressions in the same operand order (same bits): only the
-// data source of each tap changes.
+// A (32, 8) thread block owns a 32 x (8 R) x-y tile (R rows per thread) and walks a chunk of
+// z-planes.  Each thread keeps its columns' five z-values (k-2 .. k+2) in register queues; the x/y
+// neighbours of plane k come from a shared-memory tile with a 2-cell periodic halo.  Everything the
+// next plane needs -- its tile, the z-value k+3 and an auxiliary per-point input (the multigrid
+// right-hand side) -- is fetched into registers while the current plane is computed, so HBM/L2
+// latency overlaps the arithmetic; the periodic tile offsets are computed once per block.  Every
+// input value comes from HBM once per chunk (plus the tile halo, from L2) instead of once per
+// stencil tap.  The arithmetic is the generic kernels' expressions in the same operand order (same
+// bits): only the data source of each tap changes.
 #pragma once
 
 #include "common.cuh"
@@ -16,17 +17,17 @@
 
 namespace cisdc_b200 {
 
-constexpr int kTX = 32, kTY = 8, kHalo = 2;
-constexpr int kTileW = kTX + 2 * kHalo, kTileH = kTY + 2 * kHalo;
-constexpr int kTileN = kTileW * kTileH;                         // 432
-constexpr int kTilePer = (kTileN + kTX * kTY - 1) / (kTX * kTY);  // 2 elements per thread
+constexpr int kTX = 32, kTY = 8, kHalo = 2, kRows = 2;
+constexpr int kTileW = kTX + 2 * kHalo, kTileH = kTY * kRows + 2 * kHalo;
+constexpr int kTileN = kTileW * kTileH;                           // 720
+constexpr int kTilePer = (kTileN + kTX * kTY - 1) / (kTX * kTY);  // 3 elements per thread
 
 __device__ __forceinline__ int wrap_any(int x, int n) {
   x %= n;
   return x < 0 ? x + n : x;
 }
 
-// The (up to) two tile elements this thread stages: smem slot and in-plane global offset.
+// The tile elements this thread stages: smem slot and in-plane global offset.
 struct TileLoader {
   int slot[kTilePer];
   long long off[kTilePer];
@@ -73,55 +74,78 @@ __device__ __forceinline__ ZChunk zchunk(int nz, int kc) {
 #ifndef __CUDACC_RTC__
 constexpr int kZChunk = 32;
 inline dim3 tile3d_grid(int nx, int ny, int nz, int S) {
-  return dim3((unsigned)((nx + kTX - 1) / kTX), (unsigned)((ny + kTY - 1) / kTY),
+  return dim3((unsigned)((nx + kTX - 1) / kTX), (unsigned)((ny + kTY * kRows - 1) / (kTY * kRows)),
               (unsigned)(S * ((nz + kZChunk - 1) / kZChunk)));
 }
 #endif
 
-// Walks the z-chunk of one species stack f, calling body(k, v) for every in-range point with the
-// 3 x 5 taps v[axis][offset + 2] of plane k.
+using TileArr = double[kTileH][kTileW + 1];
+
+// Walks the z-chunk of one species stack f; for every in-range point calls
+// body(r, k, cell, v, aux) (r = the thread's row slot) with the 3 x 5 taps v[axis][offset + 2] of plane k and aux[cell]
+// (aux may be null: then 0).
 template <class Body>
-__device__ __forceinline__ void walk_tiled(const double* __restrict__ f, int nx, int ny, int nz, const ZChunk& z,
-                                           double (*tile)[kTileW + 1], Body body) {
-  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY;
-  const int i = i0 + threadIdx.x, j = j0 + threadIdx.y;
-  const bool in = i < nx && j < ny;
+__device__ __forceinline__ void walk_tiled(const double* __restrict__ f, const double* __restrict__ aux, int nx,
+                                           int ny, int nz, const ZChunk& z, TileArr& tile, Body body) {
+  const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY * kRows;
+  const int i = i0 + threadIdx.x;
   const long long pl = (long long)nx * ny;
-  const long long col = (long long)(in ? j : 0) * nx + (in ? i : 0);
+  bool in[kRows];
+  int jr[kRows];
+  long long col[kRows];
+  double q[kRows][5], a_nx[kRows];
+#pragma unroll
+  for (int r = 0; r < kRows; ++r) {
+    jr[r] = j0 + threadIdx.y + r * kTY;
+    in[r] = i < nx && jr[r] < ny;
+    col[r] = (long long)(in[r] ? jr[r] : 0) * nx + (in[r] ? i : 0);
+    q[r][0] = __ldg(f + wrapi(z.k0 - 2, nz) * pl + col[r]);
+    q[r][1] = __ldg(f + wrapi(z.k0 - 1, nz) * pl + col[r]);
+    q[r][2] = __ldg(f + (long long)z.k0 * pl + col[r]);
+    q[r][3] = __ldg(f + wrapi(z.k0 + 1, nz) * pl + col[r]);
+    q[r][4] = __ldg(f + wrapi(z.k0 + 2, nz) * pl + col[r]);
+    a_nx[r] = aux ? __ldg(aux + (long long)z.k0 * pl + col[r]) : 0.0;
+  }
   TileLoader L;
   L.init(nx, ny, i0, j0);
   double pre[kTilePer];
   L.fetch(f + (long long)z.k0 * pl, pre);
-  double q0 = __ldg(f + wrapi(z.k0 - 2, nz) * pl + col);
-  double q1 = __ldg(f + wrapi(z.k0 - 1, nz) * pl + col);
-  double q2 = __ldg(f + (long long)z.k0 * pl + col);
-  double q3 = __ldg(f + wrapi(z.k0 + 1, nz) * pl + col);
   L.store(&tile[0][0], pre);
-  const int tx = threadIdx.x + kHalo, ty = threadIdx.y + kHalo;
+  const int tx = threadIdx.x + kHalo;
   for (int k = z.k0; k < z.k1; ++k) {
     __syncthreads();  // tile(k) complete
-    const double q4 = __ldg(f + wrapi(k + 2, nz) * pl + col);
-    if (k + 1 < z.k1) L.fetch(f + (long long)(k + 1) * pl, pre);
-    if (in) {
+    const bool more = k + 1 < z.k1;
+    double q5[kRows], a_cur[kRows];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {  // prefetch for plane k+1
+      a_cur[r] = a_nx[r];
+      q5[r] = more ? __ldg(f + wrapi(k + 3, nz) * pl + col[r]) : 0.0;
+      if (aux && more) a_nx[r] = __ldg(aux + (long long)(k + 1) * pl + col[r]);
+    }
+    if (more) L.fetch(f + (long long)(k + 1) * pl, pre);
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      if (!in[r]) continue;
+      const int ty = threadIdx.y + r * kTY + kHalo;
       double v[3][5];
 #pragma unroll
       for (int o2 = 0; o2 < 5; ++o2) {
         v[0][o2] = tile[ty][tx + o2 - 2];
         v[1][o2] = tile[ty + o2 - 2][tx];
+        v[2][o2] = q[r][o2];
       }
-      v[2][0] = q0;
-      v[2][1] = q1;
-      v[2][2] = q2;
-      v[2][3] = q3;
-      v[2][4] = q4;
-      body(k, (long long)k * pl + col, i, j, v);
+      body(r, k, (long long)k * pl + col[r], v, a_cur[r]);
     }
     __syncthreads();  // everyone is done with tile(k)
-    if (k + 1 < z.k1) L.store(&tile[0][0], pre);
-    q0 = q1;
-    q1 = q2;
-    q2 = q3;
-    q3 = q4;
+    if (more) L.store(&tile[0][0], pre);
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      q[r][0] = q[r][1];
+      q[r][1] = q[r][2];
+      q[r][2] = q[r][3];
+      q[r][3] = q[r][4];
+      q[r][4] = q5[r];
+    }
   }
 }
 
@@ -129,15 +153,15 @@ __device__ __forceinline__ void walk_tiled(const double* __restrict__ f, int nx,
 __global__ void __launch_bounds__(kTX* kTY) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
                                                               double* __restrict__ fa, double* __restrict__ fd,
                                                               int kc) {
-  __shared__ double tile[kTileH][kTileW + 1];
+  __shared__ TileArr tile;
   const ZChunk z = zchunk(g.nz, kc);
   const double* f = phi + (long long)z.s * g.ncell;
   const long long sbase = (long long)z.s * g.ncell;
   const int s = z.s;
-  // Face velocities u_a = (T_a0[i] T_a1[j]) T_a2[k] (face_u): the (i, j) factor of the right and
-  // left faces is fixed for this thread's column -- formed once, times T_a2 per plane (same bits).
-  const int ic = min(blockIdx.x * kTX + threadIdx.x, g.nx - 1), jc = min(blockIdx.y * kTY + threadIdx.y, g.ny - 1);
-  double pr[3], pl[3];
+  // Face velocities u_a = (T_a0[i] T_a1[j]) T_a2[k] (face_u): the (i, j) factors of the right and
+  // left faces are formed once per thread-row, times T_a2 per plane (same bits as face_u).
+  const int ic = min(blockIdx.x * kTX + threadIdx.x, g.nx - 1);
+  double pr[kRows][3], pl[kRows][3];
   const double* t2[3];
   bool adv[3];
   double cd[3], ca[3];
@@ -146,35 +170,40 @@ __global__ void __launch_bounds__(kTX* kTY) k_eval_ad3_tiled(Ops o, Geom g, cons
     adv[a] = o.adv[a] != 0;
     cd[a] = o.cdiff[s][a];
     ca[a] = o.cadv[a];
-    const int il = a == 0 ? wrapi(ic - 1, g.nx) : ic, jl = a == 1 ? wrapi(jc - 1, g.ny) : jc;
+    t2[a] = o.vel[a][2];
     const double* t0 = o.vel[a][0];
     const double* t1 = o.vel[a][1];
-    pr[a] = (t0 ? __ldg(t0 + ic) : 1.0) * (t1 ? __ldg(t1 + jc) : 1.0);
-    pl[a] = (t0 ? __ldg(t0 + il) : 1.0) * (t1 ? __ldg(t1 + jl) : 1.0);
-    t2[a] = o.vel[a][2];
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      const int jc = min(blockIdx.y * kTY * kRows + threadIdx.y + r * kTY, g.ny - 1);
+      const int il = a == 0 ? wrapi(ic - 1, g.nx) : ic, jl = a == 1 ? wrapi(jc - 1, g.ny) : jc;
+      pr[r][a] = (t0 ? __ldg(t0 + ic) : 1.0) * (t1 ? __ldg(t1 + jc) : 1.0);
+      pl[r][a] = (t0 ? __ldg(t0 + il) : 1.0) * (t1 ? __ldg(t1 + jl) : 1.0);
+    }
   }
-  walk_tiled(f, g.nx, g.ny, g.nz, z, tile, [&](int k, long long cell, int, int, const double (&v)[3][5]) {
-    const long long e = sbase + cell;
-    if (fa) {
-      double acc = 0.0;
+  walk_tiled(f, nullptr, g.nx, g.ny, g.nz, z, tile,
+             [&](int r, int k, long long cell, const double (&v)[3][5], double) {
+               const long long e = sbase + cell;
+               if (fa) {
+                 double acc = 0.0;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        if (!adv[a]) continue;
-        const double ur = pr[a] * (t2[a] ? __ldg(t2[a] + k) : 1.0);
-        const double ul = pl[a] * (t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0);
-        const double fr = ur * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
-        const double fl = ul * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
-        acc = acc + (fr - fl) * ca[a];
-      }
-      fa[e] = -acc;
-    }
-    if (fd) {
-      double lap = 0.0;
+                 for (int a = 0; a < 3; ++a) {
+                   if (!adv[a]) continue;
+                   const double ur = pr[r][a] * (t2[a] ? __ldg(t2[a] + k) : 1.0);
+                   const double ul = pl[r][a] * (t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0);
+                   const double fr = ur * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
+                   const double fl = ul * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
+                   acc = acc + (fr - fl) * ca[a];
+                 }
+                 fa[e] = -acc;
+               }
+               if (fd) {
+                 double lap = 0.0;
 #pragma unroll
-      for (int a = 0; a < 3; ++a) lap = lap + cd[a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
-      fd[e] = lap;
-    }
-  });
+                 for (int a = 0; a < 3; ++a) lap = lap + cd[a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
+                 fd[e] = lap;
+               }
+             });
 }
 
 }  // namespace cisdc_b200
