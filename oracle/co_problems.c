@@ -546,6 +546,7 @@ typedef struct {
   int npass;
   double p[4], q[4];
   int reverse[4];
+  int kind[4];
   double invK;
 } circ_t;
 
@@ -560,12 +561,12 @@ static circ_t circ_factor(double c) {
     const double w1 = 2.0 + e1, w2 = 8.0 + r;
     const double z1 = 2.0 / (w1 + sqrt(e1 * (w1 + 2.0)));
     const double z2 = 2.0 / (w2 + sqrt((w2 - 2.0) * (w2 + 2.0)));
-    const double zs[4] = {z1, z2, z1, z2};
-    f.npass = 4;
-    for (int k = 0; k < 4; ++k) {
-      f.p[k] = zs[k];
-      f.q[k] = 0.0;
-      f.reverse[k] = k >= 2;
+    f.npass = 2;
+    for (int k = 0; k < 2; ++k) {
+      f.p[k] = z1;
+      f.q[k] = z2;
+      f.reverse[k] = k;
+      f.kind[k] = 1;
     }
     f.invK = (z1 * z2) / c;
   } else {
@@ -589,50 +590,90 @@ static circ_t circ_factor(double c) {
     f.q[0] = f.q[1] = zr * zr + zi * zi;
     f.reverse[0] = 0;
     f.reverse[1] = 1;
+    f.kind[0] = f.kind[1] = 0;
     f.invK = f.q[0] / c;
   }
   return f;
 }
 
 #define SCAN_T 512
+#define SCAN_NW (SCAN_T / 32)
 
-/* one periodic recurrence pass over u[0..N) with the GPU's blocking (E per thread, SCAN_T threads
-   per CTA, CL CTAs) */
-static void scan_pass(double* u, int N, int E, int CL, int reverse, double p, double q, aff_t* sc, aff_t* tmp,
-                      aff_t* excl, aff_t* tot_cta) {
-  const int nthr = CL * SCAN_T;
+/* rec_step of solve1d.cuh */
+static double rec_step(int kind, double x, double p, double q, double* s0, double* s1) {
+  if (kind == 0) {
+    const double un = (x + p * *s0) - q * *s1;
+    *s1 = *s0;
+    *s0 = un;
+    return un;
+  }
+  const double uu = x + p * *s0;
+  const double v = uu + q * *s1;
+  *s0 = uu;
+  *s1 = v;
+  return v;
+}
+
+/* one periodic recurrence pass over u[0..N) in exactly the evaluation order of solve1d.cuh
+   (periodic_pass): per-thread chain, warp Kogge-Stone scan (32 lanes), scan of the SCAN_NW warp
+   totals, cluster prefix, periodic closure, re-run */
+static void scan_pass(double* u, int N, int E, int CL, int reverse, int kind, double p, double q, aff_t* excl,
+                      aff_t* tot_cta) {
+  aff_t m[SCAN_T], incl[32], tmp[32], wtot[32], wincl[32];
   for (int rank = 0; rank < CL; ++rank) {
     for (int tid = 0; tid < SCAN_T; ++tid) {
-      const int t = rank * SCAN_T + tid;
-      const int a0 = t * E;
+      const int a0 = (rank * SCAN_T + tid) * E;
       int len = N - a0;
       if (len < 0) len = 0;
       if (len > E) len = E;
       double s0 = 0.0, s1 = 0.0, a00 = 1.0, a01 = 0.0, a10 = 0.0, a11 = 1.0;
       for (int k = 0; k < len; ++k) {
         const int e = reverse ? (len - 1 - k) : k;
-        const double un = (u[a0 + e] + p * s0) - q * s1;
-        s1 = s0;
-        s0 = un;
-        const double n00 = p * a00 - q * a10, n01 = p * a01 - q * a11;
-        a10 = a00;
-        a11 = a01;
+        rec_step(kind, u[a0 + e], p, q, &s0, &s1);
+        double n00, n01, n10, n11;
+        if (kind == 0) {
+          n00 = p * a00 - q * a10;
+          n01 = p * a01 - q * a11;
+          n10 = a00;
+          n11 = a01;
+        } else {
+          n00 = p * a00;
+          n01 = p * a01;
+          n10 = p * a00 + q * a10;
+          n11 = p * a01 + q * a11;
+        }
         a00 = n00;
         a01 = n01;
+        a10 = n10;
+        a11 = n11;
       }
-      const int pos = reverse ? (SCAN_T - 1 - tid) : tid;
-      aff_t m = {a00, a01, a10, a11, s0, s1};
-      sc[rank * SCAN_T + pos] = m;
+      aff_t mm = {a00, a01, a10, a11, s0, s1};
+      m[tid] = mm;
     }
-    aff_t* S = sc + rank * SCAN_T;
-    for (int off = 1; off < SCAN_T; off <<= 1) {
-      for (int pos = 0; pos < SCAN_T; ++pos) tmp[pos] = pos >= off ? aff_then(S[pos], S[pos - off]) : S[pos];
-      memcpy(S, tmp, sizeof(aff_t) * SCAN_T);
+    aff_t excl_lane[SCAN_T];
+    for (int warp = 0; warp < SCAN_NW; ++warp) {
+      const int wp = reverse ? SCAN_NW - 1 - warp : warp;
+      for (int lp = 0; lp < 32; ++lp) incl[lp] = m[warp * 32 + (reverse ? 31 - lp : lp)];
+      for (int off = 1; off < 32; off <<= 1) {
+        for (int lp = 0; lp < 32; ++lp) tmp[lp] = lp >= off ? aff_then(incl[lp], incl[lp - off]) : incl[lp];
+        memcpy(incl, tmp, sizeof(incl));
+      }
+      for (int lp = 0; lp < 32; ++lp) excl_lane[warp * 32 + (reverse ? 31 - lp : lp)] = lp > 0 ? incl[lp - 1] : aff_id();
+      wtot[wp] = incl[31];
     }
-    for (int pos = 0; pos < SCAN_T; ++pos) excl[rank * SCAN_T + pos] = pos > 0 ? S[pos - 1] : aff_id();
-    tot_cta[rank] = S[SCAN_T - 1];
+    for (int l = 0; l < 32; ++l) wincl[l] = l < SCAN_NW ? wtot[l] : aff_id();
+    for (int off = 1; off < 32; off <<= 1) {
+      for (int l = 0; l < 32; ++l) tmp[l] = l >= off ? aff_then(wincl[l], wincl[l - off]) : wincl[l];
+      memcpy(wincl, tmp, sizeof(wincl));
+    }
+    for (int tid = 0; tid < SCAN_T; ++tid) {
+      const int warp = tid >> 5;
+      const int wp = reverse ? SCAN_NW - 1 - warp : warp;
+      const aff_t wexcl = wp > 0 ? wincl[wp - 1] : aff_id();
+      excl[rank * SCAN_T + tid] = aff_then(excl_lane[tid], wexcl);
+    }
+    tot_cta[rank] = wincl[SCAN_NW - 1];
   }
-  (void)nthr;
   for (int rank = 0; rank < CL; ++rank) {
     const int vrank = reverse ? (CL - 1 - rank) : rank;
     aff_t pre = aff_id(), tot = aff_id();
@@ -648,21 +689,16 @@ static void scan_pass(double* u, int N, int E, int CL, int reverse, double p, do
     const double ca = pre.a00 * sa + pre.a01 * sb + pre.c0;
     const double cb = pre.a10 * sa + pre.a11 * sb + pre.c1;
     for (int tid = 0; tid < SCAN_T; ++tid) {
-      const int t = rank * SCAN_T + tid;
-      const int a0 = t * E;
+      const int a0 = (rank * SCAN_T + tid) * E;
       int len = N - a0;
       if (len < 0) len = 0;
       if (len > E) len = E;
-      const int pos = reverse ? (SCAN_T - 1 - tid) : tid;
-      const aff_t ex = excl[rank * SCAN_T + pos];
+      const aff_t ex = excl[rank * SCAN_T + tid];
       double s0 = ex.a00 * ca + ex.a01 * cb + ex.c0;
       double s1 = ex.a10 * ca + ex.a11 * cb + ex.c1;
       for (int k = 0; k < len; ++k) {
         const int e = reverse ? (len - 1 - k) : k;
-        const double un = (u[a0 + e] + p * s0) - q * s1;
-        s1 = s0;
-        s0 = un;
-        u[a0 + e] = un;
+        u[a0 + e] = rec_step(kind, u[a0 + e], p, q, &s0, &s1);
       }
     }
   }
@@ -673,9 +709,7 @@ static int adr_solve_diffusion_scan(co_problem* p, double coef, const double* rh
   int E = 1;
   while (E < 32 && (long long)E * SCAN_T * 8 < N) E *= 2;
   const int CL = (N + E * SCAN_T - 1) / (E * SCAN_T);
-  aff_t* sc = (aff_t*)malloc(sizeof(aff_t) * CL * SCAN_T);
   aff_t* ex = (aff_t*)malloc(sizeof(aff_t) * CL * SCAN_T);
-  aff_t* tmp = (aff_t*)malloc(sizeof(aff_t) * SCAN_T);
   aff_t tot[64];
   for (int s = 0; s < p->S; ++s) {
     const double* b = rhs + (size_t)s * N;
@@ -684,12 +718,10 @@ static int adr_solve_diffusion_scan(co_problem* p, double coef, const double* rh
     memcpy(o, b, sizeof(double) * N);
     if (!(coef != 0.0 && c != 0.0)) continue;
     const circ_t f = circ_factor(c);
-    for (int k = 0; k < f.npass; ++k) scan_pass(o, N, E, CL, f.reverse[k], f.p[k], f.q[k], sc, tmp, ex, tot);
+    for (int k = 0; k < f.npass; ++k) scan_pass(o, N, E, CL, f.reverse[k], f.kind[k], f.p[k], f.q[k], ex, tot);
     for (int i = 0; i < N; ++i) o[i] = o[i] * f.invK;
   }
-  free(sc);
   free(ex);
-  free(tmp);
   return CISDC_OK;
 }
 

@@ -18,10 +18,13 @@ namespace cisdc_b200 {
 // (backward), then y = invK * u.  Real roots (c > 1/36, the stiff case) are applied as four
 // first-order passes (q = 0) so that 1 - zeta carries full relative precision for the slowly
 // decaying constant mode; a complex-conjugate pair as one second-order pass per direction.
+// Real roots: one forward and one backward pass, each running the two first-order recurrences
+// (zeta1 then zeta2) coupled in a single scan (kind 1).
 struct CircFactor {
   int npass;
   double p[4], q[4];
   int reverse[4];
+  int kind[4];
   double invK;
 };
 
@@ -35,12 +38,12 @@ inline CircFactor factor_circulant(double c) {
     const double w1 = 2.0 + e1, w2 = 8.0 + r;
     const double z1 = 2.0 / (w1 + std::sqrt(e1 * (w1 + 2.0)));
     const double z2 = 2.0 / (w2 + std::sqrt((w2 - 2.0) * (w2 + 2.0)));
-    f.npass = 4;
-    const double zs[4] = {z1, z2, z1, z2};
-    for (int k = 0; k < 4; ++k) {
-      f.p[k] = zs[k];
-      f.q[k] = 0.0;
-      f.reverse[k] = k >= 2;
+    f.npass = 2;
+    for (int k = 0; k < 2; ++k) {
+      f.p[k] = z1;
+      f.q[k] = z2;
+      f.reverse[k] = k;
+      f.kind[k] = 1;
     }
     f.invK = (z1 * z2) / c;
   } else {
@@ -66,6 +69,7 @@ inline CircFactor factor_circulant(double c) {
     f.q[0] = f.q[1] = zr * zr + zi * zi;
     f.reverse[0] = 0;
     f.reverse[1] = 1;
+    f.kind[0] = f.kind[1] = 0;
     f.invK = f.q[0] / c;
   }
   return f;

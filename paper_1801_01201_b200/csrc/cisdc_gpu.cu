@@ -450,6 +450,7 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
         a.c[sp].p[k] = f.p[k];
         a.c[sp].q[k] = f.q[k];
         a.c[sp].reverse[k] = f.reverse[k];
+        a.c[sp].kind[k] = f.kind[k];
       }
       a.c[sp].invK = f.invK;
     }

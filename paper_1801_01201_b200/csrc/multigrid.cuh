@@ -179,7 +179,7 @@ __device__ __forceinline__ double mg_ax_taps(const MgCoef& C, int s, const doubl
 
 // mode 0: smooth x -> xo (not from zero); mode 1: residual inf-norm into out[s]
 template <int MODE>
-__global__ void __launch_bounds__(kTX* kTY) k_mg3_tiled(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+__global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                          const double* __restrict__ b, double* __restrict__ xo,
                                                          int nx, int ny, int nz, int kc, const int* __restrict__ active,
                                                          double* __restrict__ out) {

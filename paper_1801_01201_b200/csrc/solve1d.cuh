@@ -32,6 +32,7 @@ struct Circ {
   int npass;
   double p[4], q[4];
   int reverse[4];
+  int kind[4];  // 0: second-order (p, q); 1: two coupled first-order (zeta1 = p, zeta2 = q)
   double invK;
 };
 
@@ -63,22 +64,54 @@ __device__ __forceinline__ Aff aff_then(const Aff& later, const Aff& earlier) {
 
 template <int T>
 struct Solve1dSmem {
-  Aff scan[T];
-  Aff total[4];  // per pass: this CTA's total map (read by the cluster peers through DSMEM)
+  Aff wtot[T / 32];   // warp totals (visiting order)
+  Aff wincl[T / 32];  // their inclusive scan
+  Aff peer[16];       // CTA totals of the cluster, by rank
+  Aff total[4];       // per pass: this CTA's total map (read by the cluster peers through DSMEM)
 };
 
-// One pass of the periodic recurrence u_i = (x_i + p u_{i-1}) - q u_{i-2} in visiting order.
-// pos: this thread's scan position; ranks in visiting order.
+__device__ __forceinline__ double shfl_dir(double v, int delta, bool down) {
+  return down ? __shfl_down_sync(0xffffffffu, v, delta) : __shfl_up_sync(0xffffffffu, v, delta);
+}
+__device__ __forceinline__ Aff shfl_aff(const Aff& m, int delta, bool down) {
+  return {shfl_dir(m.a00, delta, down), shfl_dir(m.a01, delta, down), shfl_dir(m.a10, delta, down),
+          shfl_dir(m.a11, delta, down), shfl_dir(m.c0, delta, down),  shfl_dir(m.c1, delta, down)};
+}
+
+// One step of a pass's recurrence on the state (s0, s1); returns the element's new value.
+//   kind 0 (second order):        u = (x + p s0) - q s1;           state (u_i, u_{i-1})
+//   kind 1 (two coupled 1st order): u = x + p s0; v = u + q s1;   state (u_i, v_i), output v
+__device__ __forceinline__ double rec_step(int kind, double x, double p, double q, double& s0, double& s1) {
+  if (kind == 0) {
+    const double un = (x + p * s0) - q * s1;
+    s1 = s0;
+    s0 = un;
+    return un;
+  }
+  const double u = x + p * s0;
+  const double v = u + q * s1;
+  s0 = u;
+  s1 = v;
+  return v;
+}
+
+// One pass of a periodic recurrence over the cluster's elements in visiting order (reverse = from
+// the last element down).  Scan of 2x2 affine maps: thread-local chain -> warp Kogge-Stone scan
+// (shuffles) -> scan of the warp totals -> cluster prefix from the CTA totals (DSMEM) -> periodic
+// closure s_{-1} = (I - A_N)^{-1} c_N -> re-run of the chain from the exact incoming state.
+// oracle/co_problems.c (scan_pass) emulates this evaluation order exactly.
 template <int E, int T>
-__device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reverse, double p, double q,
+__device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reverse, int kind, double p, double q,
                                               Solve1dSmem<T>& sm, int pass, cg::cluster_group& cluster,
                                               int cl_size) {
-  const int tid = threadIdx.x;
-  const int pos = reverse ? (T - 1 - tid) : tid;
+  constexpr int NW = T / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lp = reverse ? 31 - lane : lane;
+  const int wp = reverse ? NW - 1 - warp : warp;
   const int my_rank = static_cast<int>(cluster.block_rank());
   const int vrank = reverse ? (cl_size - 1 - my_rank) : my_rank;
   // local map with zero incoming state
-  Aff m = aff_identity();
+  Aff m;
   {
     double s0 = 0.0, s1 = 0.0;
     double a00 = 1.0, a01 = 0.0, a10 = 0.0, a11 = 1.0;
@@ -86,42 +119,61 @@ __device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reve
     for (int t = 0; t < E; ++t) {
       if (t < len) {
         const int e = reverse ? (len - 1 - t) : t;
-        const double un = (u[e] + p * s0) - q * s1;
-        s1 = s0;
-        s0 = un;
-        // A <- T A, T = [[p, -q], [1, 0]]
-        const double n00 = p * a00 - q * a10, n01 = p * a01 - q * a11;
-        a10 = a00;
-        a11 = a01;
+        rec_step(kind, u[e], p, q, s0, s1);
+        double n00, n01, n10, n11;
+        if (kind == 0) {  // A <- [[p, -q], [1, 0]] A
+          n00 = p * a00 - q * a10;
+          n01 = p * a01 - q * a11;
+          n10 = a00;
+          n11 = a01;
+        } else {  // A <- [[p, 0], [p, q]] A
+          n00 = p * a00;
+          n01 = p * a01;
+          n10 = p * a00 + q * a10;
+          n11 = p * a01 + q * a11;
+        }
         a00 = n00;
         a01 = n01;
+        a10 = n10;
+        a11 = n11;
       }
     }
     m = {a00, a01, a10, a11, s0, s1};
   }
-  // inclusive Hillis-Steele scan over positions within the CTA
-  sm.scan[pos] = m;
-  __syncthreads();
-  for (int off = 1; off < T; off <<= 1) {
-    Aff other = aff_identity();
-    const bool has = pos >= off;
-    if (has) other = sm.scan[pos - off];
-    __syncthreads();
-    if (has) {
-      m = aff_then(m, other);
-      sm.scan[pos] = m;
-    }
-    __syncthreads();
+  // warp inclusive scan over lane positions lp
+  Aff incl = m;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const Aff o = shfl_aff(incl, off, reverse);
+    if (lp >= off) incl = aff_then(incl, o);
   }
-  const Aff excl = pos > 0 ? sm.scan[pos - 1] : aff_identity();
-  if (pos == T - 1) sm.total[pass] = m;
+  Aff excl_lane = shfl_aff(incl, 1, reverse);
+  if (lp == 0) excl_lane = aff_identity();
+  if (lp == 31) sm.wtot[wp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    Aff w = lane < NW ? sm.wtot[lane] : aff_identity();
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const Aff o = shfl_aff(w, off, false);
+      if (lane >= off) w = aff_then(w, o);
+    }
+    if (lane < NW) sm.wincl[lane] = w;
+  }
+  __syncthreads();
+  const Aff wexcl = wp > 0 ? sm.wincl[wp - 1] : aff_identity();
+  const Aff excl = aff_then(excl_lane, wexcl);
+  if (tid == 0) sm.total[pass] = sm.wincl[NW - 1];
   cluster.sync();
+  if (tid < cl_size) {
+    Solve1dSmem<T>* peer = cluster.map_shared_rank(&sm, tid);
+    sm.peer[tid] = peer->total[pass];
+  }
+  __syncthreads();
   // cluster prefix (CTAs before me in visiting order) and global total
   Aff pre = aff_identity(), tot = aff_identity();
   for (int v = 0; v < cl_size; ++v) {
-    const int r = reverse ? (cl_size - 1 - v) : v;
-    Solve1dSmem<T>* peer = cluster.map_shared_rank(&sm, r);
-    const Aff tv = peer->total[pass];
+    const Aff tv = sm.peer[reverse ? (cl_size - 1 - v) : v];
     if (v < vrank) pre = aff_then(tv, pre);
     tot = aff_then(tv, tot);
   }
@@ -139,10 +191,7 @@ __device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reve
   for (int t = 0; t < E; ++t) {
     if (t < len) {
       const int e = reverse ? (len - 1 - t) : t;
-      const double un = (u[e] + p * s0) - q * s1;
-      s1 = s0;
-      s0 = un;
-      u[e] = un;
+      u[e] = rec_step(kind, u[e], p, q, s0, s1);
     }
   }
 }
@@ -170,7 +219,7 @@ __global__ void __launch_bounds__(T) k_solve1d_periodic(const __grid_constant__ 
 #pragma unroll
   for (int t = 0; t < E; ++t) u[t] = t < len ? b[a0 + t] : 0.0;
   for (int k = 0; k < c.npass; ++k)
-    periodic_pass<E, T>(u, len, c.reverse[k] != 0, c.p[k], c.q[k], sm, k, cluster, cl_size);
+    periodic_pass<E, T>(u, len, c.reverse[k] != 0, c.kind[k], c.p[k], c.q[k], sm, k, cluster, cl_size);
 #pragma unroll
   for (int t = 0; t < E; ++t)
     if (t < len) y[a0 + t] = u[t] * c.invK;

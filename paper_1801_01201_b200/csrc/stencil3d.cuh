@@ -81,6 +81,9 @@ inline dim3 tile3d_grid(int nx, int ny, int nz, int S) {
 
 using TileArr = double[kTileH][kTileW + 1];
 
+// occupancy targets (blocks of 256 per SM): the kernels are latency-bound on dependent FP64 chains
+constexpr int kEvalMinBlocks = 3, kMgMinBlocks = 4;
+
 // Walks the z-chunk of one species stack f; for every in-range point calls
 // body(r, k, cell, v, aux) (r = the thread's row slot) with the 3 x 5 taps v[axis][offset + 2] of plane k and aux[cell]
 // (aux may be null: then 0).
@@ -150,7 +153,7 @@ __device__ __forceinline__ void walk_tiled(const double* __restrict__ f, const d
 }
 
 // F_A and/or F_D, 3-D periodic
-__global__ void __launch_bounds__(kTX* kTY) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
+__global__ void __launch_bounds__(kTX* kTY, kEvalMinBlocks) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
                                                               double* __restrict__ fa, double* __restrict__ fd,
                                                               int kc) {
   __shared__ TileArr tile;
