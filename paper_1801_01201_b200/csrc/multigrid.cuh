@@ -97,8 +97,10 @@ __global__ void k_mg_absmax(const double* __restrict__ b, long long ncell, doubl
 template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_resmax(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                    const double* __restrict__ b, int nx, int ny, int nz,
-                                                   const int* __restrict__ active, double* __restrict__ out) {
+                                                   const int* __restrict__ active, double* __restrict__ out,
+                                                   double* __restrict__ bmax) {
   __shared__ double red[8];
+  __shared__ double redb[8];
   const int s = blockIdx.z;
   if (!active[s]) return;  // uniform per block
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -106,19 +108,42 @@ __global__ void __launch_bounds__(256) k_mg_resmax(const __grid_constant__ MgCoe
   const long long ncell = (long long)nx * ny * nz;
   const double* xs = x + (long long)s * ncell;
   const double* bs = b + (long long)s * ncell;
-  double m = 0.0;
+  double m = 0.0, mb = 0.0;
   if (i < nx && j < ny)
-    for (int k = 0; k < nz; ++k)
-      m = fmax(m, fabs(bs[((long long)k * ny + j) * nx + i] - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k)));
+    for (int k = 0; k < nz; ++k) {
+      const double bv = bs[((long long)k * ny + j) * nx + i];
+      m = fmax(m, fabs(bv - mg_ax<DIM>(C, s, xs, nx, ny, nz, i, j, k)));
+      mb = fmax(mb, fabs(bv));
+    }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+  for (int off = 16; off > 0; off >>= 1) {
+    m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+    mb = fmax(mb, __shfl_down_sync(0xffffffffu, mb, off));
+  }
   const int t = threadIdx.y * blockDim.x + threadIdx.x;
-  if ((t & 31) == 0) red[t >> 5] = m;
+  if ((t & 31) == 0) {
+    red[t >> 5] = m;
+    redb[t >> 5] = mb;
+  }
   __syncthreads();
   if (t == 0) {
-    for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) m = fmax(m, red[w]);
+    for (int w = 1; w < (int)(blockDim.x * blockDim.y) / 32; ++w) {
+      m = fmax(m, red[w]);
+      mb = fmax(mb, redb[w]);
+    }
     if (m > 0.0) atomic_max_nonneg(out + s, m);
+    if (bmax && mb > 0.0) atomic_max_nonneg(bmax + s, mb);
   }
+}
+
+// out = b for the species that needed no cycle (x = b met the tolerance)
+__global__ void k_mg_copy_unswept(const double* __restrict__ b, double* __restrict__ out, long long ncell,
+                                  const int* __restrict__ cycles) {
+  const int s = blockIdx.y;
+  if (cycles[s] != 0) return;
+  const long long base = (long long)s * ncell;
+  for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += (long long)gridDim.x * blockDim.x)
+    out[base + c] = b[base + c];
 }
 
 // per-species stop decision of the oracle's loop: rn <= tol*bn -> done; cap -> failure
@@ -182,9 +207,10 @@ template <int MODE>
 __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                          const double* __restrict__ b, double* __restrict__ xo,
                                                          int nx, int ny, int nz, int kc, const int* __restrict__ active,
-                                                         double* __restrict__ out) {
+                                                         double* __restrict__ out, double* __restrict__ bmax) {
   __shared__ TileArr tile;
   __shared__ double red[kTX * kTY / 32];
+  __shared__ double redb[kTX * kTY / 32];
   const ZChunk z = zchunk(nz, kc);
   if (!active[z.s]) return;  // uniform per block
   const long long ncell = (long long)nx * ny * nz;
@@ -192,7 +218,7 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
   const double* f = x + sbase;
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
-  double m = 0.0;
+  double m = 0.0, mb = 0.0;
   walk_tiled(f, b + sbase, nx, ny, nz, z, tile, [&](int, int, long long cell, const double (&v)[3][5], double bv) {
     // mg_ax_taps with the species coefficients hoisted (same expression)
     double lap = 0.0;
@@ -200,18 +226,32 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
     lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
     lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
     const double r = bv - (v[0][2] - coef * lap);
-    if (MODE == 0) xo[sbase + cell] = v[2][2] + wd * r;
-    else m = fmax(m, fabs(r));
+    if (MODE == 0) {
+      xo[sbase + cell] = v[2][2] + wd * r;
+    } else {
+      m = fmax(m, fabs(r));
+      mb = fmax(mb, fabs(bv));
+    }
   });
   if (MODE == 1) {
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+    for (int off = 16; off > 0; off >>= 1) {
+      m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
+      mb = fmax(mb, __shfl_down_sync(0xffffffffu, mb, off));
+    }
     const int t = threadIdx.y * kTX + threadIdx.x;
-    if ((t & 31) == 0) red[t >> 5] = m;
+    if ((t & 31) == 0) {
+      red[t >> 5] = m;
+      redb[t >> 5] = mb;
+    }
     __syncthreads();
     if (t == 0) {
-      for (int w = 1; w < kTX * kTY / 32; ++w) m = fmax(m, red[w]);
+      for (int w = 1; w < kTX * kTY / 32; ++w) {
+        m = fmax(m, red[w]);
+        mb = fmax(mb, redb[w]);
+      }
       if (m > 0.0) atomic_max_nonneg(out + z.s, m);
+      if (bmax && mb > 0.0) atomic_max_nonneg(bmax + z.s, mb);
     }
   }
 }
@@ -387,6 +427,7 @@ struct MgRunner {
   // level-0 x lives in h.lv[0].x (ping-pong with .t); b0 = rhs.  Sweep counts are even, so after
   // every pair of sweeps .x holds the iterate again for active AND masked (converged) species.
   const double* b0;
+  const double* first_x = nullptr;  // the initial iterate x = b is read straight from the rhs
 
   const double* bof(int l) const { return l == 0 ? b0 : h.lv[l].b; }
   dim3 grid(const MgLevel& Lv) const { return stencil_grid(Lv.nx, Lv.ny, Lv.nz, h.S, DIM); }
@@ -394,12 +435,14 @@ struct MgRunner {
 
   void smooth(int l, bool from_zero) {
     MgLevel& Lv = h.lv[l];
+    const double* xin = (l == 0 && first_x) ? first_x : Lv.x;
+    if (l == 0) first_x = nullptr;
     hook->before(kKMgSmooth, s);
     if (DIM == 3 && !from_zero)
       k_mg3_tiled<0><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
-          C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, nullptr);
+          C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, nullptr, nullptr);
     else
-      k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
+      k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
                                                     h.d_active);
     hook->after(kKMgSmooth, s, 8.0 * Lv.ncell * h.S * (from_zero ? 2 : 3));
     std::swap(Lv.x, Lv.t);
@@ -441,12 +484,15 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   cudaMemsetAsync(h.d_bmax, 0, sizeof(double) * g.S, s);
   cudaMemsetAsync(h.d_rmax, 0, sizeof(double) * g.S, s);
   cudaMemsetAsync(h.d_flag, 0, sizeof(int) * 2, s);
+  // Level 0 iterates directly in `out` (ping-pong with the level-0 workspace; even sweep counts
+  // leave the iterate in `out`), and the initial iterate x = b is read straight from the rhs:
+  // no copy in, no copy out.
   MgLevel& L0 = h.lv[0];
-  cudaMemcpyAsync(L0.x, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);  // x = b
-  const dim3 rgrid((unsigned)std::min<long long>((g.ncell + 255) / 256, 1184), (unsigned)g.S, 1);
-  hook->before(kKMgNorm, s);
-  k_mg_absmax<<<rgrid, 256, 0, s>>>(rhs, g.ncell, h.d_bmax);
-  hook->after(kKMgNorm, s, 8.0 * n);
+  double* own_x = L0.x;
+  double* own_t = L0.t;
+  L0.x = out;
+  R.first_x = rhs;
+  const double* x_check = rhs;  // the first check sees x = b (and also forms ||b||_inf)
   // The host enqueues cycles in batches (predicted from the last solve with this coefficient) and
   // only then looks at the device flag: cycles past convergence are masked no-ops, so the result
   // is identical to checking after every cycle.
@@ -458,12 +504,14 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     hook->before(kKMgNorm, s);
     const dim3 rb = R.block();
     const dim3 rg((L0.nx + rb.x - 1) / rb.x, (L0.ny + rb.y - 1) / rb.y, g.S);
+    double* bmax = x_check == rhs ? h.d_bmax : nullptr;
     if (DIM == 3)
       k_mg3_tiled<1><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
-          R.C[0], L0.x, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax);
+          R.C[0], x_check, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax, bmax);
     else
-      k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], L0.x, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax);
-    hook->after(kKMgNorm, s, 16.0 * n);
+      k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], x_check, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax, bmax);
+    hook->after(kKMgNorm, s, (x_check == rhs ? 8.0 : 16.0) * n);
+    x_check = L0.x;
     hook->before(kKMgNorm, s);
     k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
                                  h.d_flag, st);
@@ -500,7 +548,13 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     if (h.predicted.size() >= 64) h.predicted.erase(h.predicted.begin());
     h.predicted.push_back({coef, used});
   }
-  if (cudaMemcpyAsync(out, L0.x, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
+  const bool in_out = L0.x == out;
+  L0.x = own_x;
+  L0.t = own_t;
+  if (!in_out) return CISDC_E_CUDA;  // unreachable with even sweep counts
+  // species that met the tolerance at x = b never had a sweep write `out`
+  const dim3 cg((unsigned)std::min<long long>((g.ncell + 255) / 256, 4096), (unsigned)g.S, 1);
+  k_mg_copy_unswept<<<cg, 256, 0, s>>>(rhs, out, g.ncell, h.d_cycles);
   if (cudaGetLastError() != cudaSuccess) return CISDC_E_CUDA;
   return CISDC_OK;
 }

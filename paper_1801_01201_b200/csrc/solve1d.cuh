@@ -100,8 +100,8 @@ __device__ __forceinline__ double rec_step(int kind, double x, double p, double 
 // (shuffles) -> scan of the warp totals -> cluster prefix from the CTA totals (DSMEM) -> periodic
 // closure s_{-1} = (I - A_N)^{-1} c_N -> re-run of the chain from the exact incoming state.
 // oracle/co_problems.c (scan_pass) emulates this evaluation order exactly.
-template <int E, int T>
-__device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reverse, int kind, double p, double q,
+template <int E, int T, bool reverse>
+__device__ __forceinline__ void periodic_pass(double (&u)[E], int len, int kind, double p, double q,
                                               Solve1dSmem<T>& sm, int pass, cg::cluster_group& cluster,
                                               int cl_size) {
   constexpr int NW = T / 32;
@@ -110,16 +110,17 @@ __device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reve
   const int wp = reverse ? NW - 1 - warp : warp;
   const int my_rank = static_cast<int>(cluster.block_rank());
   const int vrank = reverse ? (cl_size - 1 - my_rank) : my_rank;
-  // local map with zero incoming state
+  // local map with zero incoming state (element index t is a compile-time constant in both
+  // directions, so u[] stays in registers)
   Aff m;
   {
     double s0 = 0.0, s1 = 0.0;
     double a00 = 1.0, a01 = 0.0, a10 = 0.0, a11 = 1.0;
 #pragma unroll
-    for (int t = 0; t < E; ++t) {
+    for (int tt = 0; tt < E; ++tt) {
+      const int t = reverse ? (E - 1 - tt) : tt;
       if (t < len) {
-        const int e = reverse ? (len - 1 - t) : t;
-        rec_step(kind, u[e], p, q, s0, s1);
+        rec_step(kind, u[t], p, q, s0, s1);
         double n00, n01, n10, n11;
         if (kind == 0) {  // A <- [[p, -q], [1, 0]] A
           n00 = p * a00 - q * a10;
@@ -163,13 +164,18 @@ __device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reve
   __syncthreads();
   const Aff wexcl = wp > 0 ? sm.wincl[wp - 1] : aff_identity();
   const Aff excl = aff_then(excl_lane, wexcl);
-  if (tid == 0) sm.total[pass] = sm.wincl[NW - 1];
-  cluster.sync();
-  if (tid < cl_size) {
-    Solve1dSmem<T>* peer = cluster.map_shared_rank(&sm, tid);
-    sm.peer[tid] = peer->total[pass];
+  if (cl_size == 1) {  // single CTA: no cluster barrier, no DSMEM
+    if (tid == 0) sm.peer[0] = sm.wincl[NW - 1];
+    __syncthreads();
+  } else {
+    if (tid == 0) sm.total[pass] = sm.wincl[NW - 1];
+    cluster.sync();
+    if (tid < cl_size) {
+      Solve1dSmem<T>* peer = cluster.map_shared_rank(&sm, tid);
+      sm.peer[tid] = peer->total[pass];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   // cluster prefix (CTAs before me in visiting order) and global total
   Aff pre = aff_identity(), tot = aff_identity();
   for (int v = 0; v < cl_size; ++v) {
@@ -188,11 +194,9 @@ __device__ __forceinline__ void periodic_pass(double (&u)[E], int len, bool reve
   double s0 = excl.a00 * ca + excl.a01 * cb + excl.c0;
   double s1 = excl.a10 * ca + excl.a11 * cb + excl.c1;
 #pragma unroll
-  for (int t = 0; t < E; ++t) {
-    if (t < len) {
-      const int e = reverse ? (len - 1 - t) : t;
-      u[e] = rec_step(kind, u[e], p, q, s0, s1);
-    }
+  for (int tt = 0; tt < E; ++tt) {
+    const int t = reverse ? (E - 1 - tt) : tt;
+    if (t < len) u[t] = rec_step(kind, u[t], p, q, s0, s1);
   }
 }
 
@@ -219,11 +223,12 @@ __global__ void __launch_bounds__(T) k_solve1d_periodic(const __grid_constant__ 
 #pragma unroll
   for (int t = 0; t < E; ++t) u[t] = t < len ? b[a0 + t] : 0.0;
   for (int k = 0; k < c.npass; ++k)
-    periodic_pass<E, T>(u, len, c.reverse[k] != 0, c.kind[k], c.p[k], c.q[k], sm, k, cluster, cl_size);
+    if (c.reverse[k]) periodic_pass<E, T, true>(u, len, c.kind[k], c.p[k], c.q[k], sm, k, cluster, cl_size);
+    else periodic_pass<E, T, false>(u, len, c.kind[k], c.p[k], c.q[k], sm, k, cluster, cl_size);
 #pragma unroll
   for (int t = 0; t < E; ++t)
     if (t < len) y[a0 + t] = u[t] * c.invK;
-  cluster.sync();  // peers may still read this CTA's totals through DSMEM
+  if (cl_size > 1) cluster.sync();  // peers may still read this CTA's totals through DSMEM
 }
 
 // Reference Dirichlet system, one thread (bit-identical to assemble_diffusion_system + banded_solve)

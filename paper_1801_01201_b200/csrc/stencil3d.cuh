@@ -81,8 +81,9 @@ inline dim3 tile3d_grid(int nx, int ny, int nz, int S) {
 
 using TileArr = double[kTileH][kTileW + 1];
 
-// occupancy targets (blocks of 256 per SM): the kernels are latency-bound on dependent FP64 chains
-constexpr int kEvalMinBlocks = 3, kMgMinBlocks = 4;
+// occupancy targets (blocks of 256 per SM); forcing more resident blocks spills and was measured
+// slower (C5: F_A/F_D 1.6 -> 2.0 ms per launch at 3 blocks)
+constexpr int kEvalMinBlocks = 1, kMgMinBlocks = 1;
 
 // Walks the z-chunk of one species stack f; for every in-range point calls
 // body(r, k, cell, v, aux) (r = the thread's row slot) with the 3 x 5 taps v[axis][offset + 2] of plane k and aux[cell]
