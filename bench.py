@@ -226,8 +226,13 @@ def main():
     d_out = torch.empty_like(d_phi0)
     torch.cuda.synchronize()
 
-    def step_device():
-        ctx.check(lib.cisdc_gpu_integrate_device(ctx.h, C.c_void_p(d_phi0.data_ptr()), n, C.byref(oc),
+    # the per-kernel breakdown pass runs the sweeps on one stream (workers <= 1) so that the event
+    # intervals of different kernel classes never overlap
+    oc1 = api.IntegrateOptions(scheme=scheme, dt=spec.dt, n_steps=1, M=spec.M, n_sweeps=spec.n_sweeps, nu=spec.nu,
+                               workers=min(workers, 1), convention=spec.convention).to_c()
+
+    def step_device(o=oc):
+        ctx.check(lib.cisdc_gpu_integrate_device(ctx.h, C.c_void_p(d_phi0.data_ptr()), n, C.byref(o),
                                                  C.c_void_p(d_out.data_ptr()), C.byref(rep), _abi.dptr(incs)))
         return rep.counters.newton_iterations
 
@@ -237,8 +242,10 @@ def main():
 
     for _ in range(args.warmup):
         step_device()
+    # timed region: per-kernel events off (they would add host work per launch on the small,
+    # launch-bound configs); launches are counted regardless
     lib.cisdc_gpu_kernel_times(ctx.h, None, None, None, 0, 1)  # reset
-    lib.cisdc_gpu_set_timing(ctx.h, 1)
+    lib.cisdc_gpu_device_time_ms(ctx.h, 1)
     newton = 0
     barrier(ws)
     torch.cuda.synchronize()
@@ -247,14 +254,23 @@ def main():
             newton += step_device()
         torch.cuda.synchronize()
     barrier(ws)
-    dev_ms = lib.cisdc_gpu_device_time_ms(ctx.h, 0)
+    dev_ms = lib.cisdc_gpu_device_time_ms(ctx.h, 1)
+    launches = int(lib.cisdc_gpu_launch_count(ctx.h))  # our kernels launched in the timed region
+    tmax = max_over_ranks(ws, dev_ms)
+
+    # the same K steps again with live CUDA-event timing of every launch, per kernel class, on the
+    # stream each kernel is launched on (roofline + breakdown)
+    lib.cisdc_gpu_kernel_times(ctx.h, None, None, None, 0, 1)
+    lib.cisdc_gpu_set_timing(ctx.h, 1)
+    for _ in range(args.steps):
+        step_device(oc1)
+    torch.cuda.synchronize()
+    inst_ms = lib.cisdc_gpu_device_time_ms(ctx.h, 1)
     ms = (C.c_double * 16)()
     by = (C.c_double * 16)()
     cnt = (C.c_longlong * 16)()
-    launches = int(lib.cisdc_gpu_launch_count(ctx.h))  # our kernels launched in the timed region
     ncls = lib.cisdc_gpu_kernel_times(ctx.h, ms, by, cnt, 16, 1)
     lib.cisdc_gpu_set_timing(ctx.h, 0)
-    tmax = max_over_ranks(ws, dev_ms)
     updates_per_step = n * spec.M * spec.n_sweeps
     value = ws * updates_per_step * args.steps / (tmax * 1e-3)
 
@@ -322,6 +338,8 @@ def main():
             "gpu_launches": launches,
             "roofline": roof,
             "kernels": sorted(classes, key=lambda x: -x["ms"]),
+            "kernels_pass": {"ms_per_step": inst_ms / args.steps, "workers": min(workers, 1),
+                             "note": "per-kernel CUDA-event pass, same K steps, one stream"},
             "end_to_end_hbm": {"algorithmic_bytes_per_sweep": 8.0 * n * (7 * spec.M + 4),
                                "achieved_gbs": 8.0 * n * (7 * spec.M + 4) * spec.n_sweeps * args.steps / (tmax * 1e-3) / 1e9},
             "newton_trips_per_cell_solve": newton / max(cell_solves, 1),

@@ -211,6 +211,10 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
     case 1: k_eval_ad<1><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
     case 2: k_eval_ad<2><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
     default:
+      if (!tile3d_ok(g.ncell)) {
+        k_eval_ad<3><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd);
+        break;
+      }
       k_eval_ad3_tiled<<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa, fd,
                                                                                       kZChunk);
       break;

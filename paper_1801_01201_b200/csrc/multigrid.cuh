@@ -202,7 +202,11 @@ __device__ __forceinline__ double mg_ax_taps(const MgCoef& C, int s, const doubl
   return v[0][2] - C.coef * lap;
 }
 
-// mode 0: smooth x -> xo (not from zero); mode 1: residual inf-norm into out[s]
+// max of non-negative values, NaN ignored (the oracle's `if (r > m) m = r`)
+__device__ __forceinline__ double max_keep(double m, double r) { return r > m ? r : m; }
+
+// mode 0: smooth x -> xo (not from zero); mode 1: residual inf-norm into out[s]; mode 2: also
+// ||b||_inf into bmax[s]
 template <int MODE>
 __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                          const double* __restrict__ b, double* __restrict__ xo,
@@ -215,29 +219,30 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
   if (!active[z.s]) return;  // uniform per block
   const long long ncell = (long long)nx * ny * nz;
   const long long sbase = (long long)z.s * ncell;
-  const double* f = x + sbase;
+  double* xos = MODE == 0 ? opaque(xo + sbase) : nullptr;
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_tiled(f, b + sbase, nx, ny, nz, z, tile, [&](int, int, long long cell, const double (&v)[3][5], double bv) {
-    // mg_ax_taps with the species coefficients hoisted (same expression)
-    double lap = 0.0;
-    lap = lap + cs0 * (-v[0][0] + 16.0 * v[0][1] - 30.0 * v[0][2] + 16.0 * v[0][3] - v[0][4]);
-    lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
-    lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
-    const double r = bv - (v[0][2] - coef * lap);
-    if (MODE == 0) {
-      xo[sbase + cell] = v[2][2] + wd * r;
-    } else {
-      m = fmax(m, fabs(r));
-      mb = fmax(mb, fabs(bv));
-    }
-  });
-  if (MODE == 1) {
+  walk_tiled(x + sbase, b + sbase, nx, ny, nz, z, tile, [](int) {},
+             [&](int, int, unsigned cell, const double (&v)[3][5], double bv, bool ok) {
+               // mg_ax_taps with the species coefficients hoisted (same expression)
+               double lap = 0.0;
+               lap = lap + cs0 * (-v[0][0] + 16.0 * v[0][1] - 30.0 * v[0][2] + 16.0 * v[0][3] - v[0][4]);
+               lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
+               lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
+               const double r = bv - (v[0][2] - coef * lap);
+               if (MODE == 0) {
+                 if (ok) xos[cell] = v[2][2] + wd * r;
+               } else if (ok) {
+                 m = max_keep(m, fabs(r));
+                 if (MODE == 2) mb = max_keep(mb, fabs(bv));
+               }
+             });
+  if (MODE >= 1) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-      m = fmax(m, __shfl_down_sync(0xffffffffu, m, off));
-      mb = fmax(mb, __shfl_down_sync(0xffffffffu, mb, off));
+      m = max_keep(m, __shfl_down_sync(0xffffffffu, m, off));
+      if (MODE == 2) mb = max_keep(mb, __shfl_down_sync(0xffffffffu, mb, off));
     }
     const int t = threadIdx.y * kTX + threadIdx.x;
     if ((t & 31) == 0) {
@@ -247,11 +252,11 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
     __syncthreads();
     if (t == 0) {
       for (int w = 1; w < kTX * kTY / 32; ++w) {
-        m = fmax(m, red[w]);
-        mb = fmax(mb, redb[w]);
+        m = max_keep(m, red[w]);
+        mb = max_keep(mb, redb[w]);
       }
       if (m > 0.0) atomic_max_nonneg(out + z.s, m);
-      if (bmax && mb > 0.0) atomic_max_nonneg(bmax + z.s, mb);
+      if (MODE == 2 && mb > 0.0) atomic_max_nonneg(bmax + z.s, mb);
     }
   }
 }
@@ -438,7 +443,7 @@ struct MgRunner {
     const double* xin = (l == 0 && first_x) ? first_x : Lv.x;
     if (l == 0) first_x = nullptr;
     hook->before(kKMgSmooth, s);
-    if (DIM == 3 && !from_zero)
+    if (DIM == 3 && !from_zero && tile3d_ok(Lv.ncell))
       k_mg3_tiled<0><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
           C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, nullptr, nullptr);
     else
@@ -505,9 +510,12 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     const dim3 rb = R.block();
     const dim3 rg((L0.nx + rb.x - 1) / rb.x, (L0.ny + rb.y - 1) / rb.y, g.S);
     double* bmax = x_check == rhs ? h.d_bmax : nullptr;
-    if (DIM == 3)
-      k_mg3_tiled<1><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
+    if (DIM == 3 && tile3d_ok(L0.ncell) && bmax)
+      k_mg3_tiled<2><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
           R.C[0], x_check, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax, bmax);
+    else if (DIM == 3 && tile3d_ok(L0.ncell))
+      k_mg3_tiled<1><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
+          R.C[0], x_check, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax, nullptr);
     else
       k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], x_check, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax, bmax);
     hook->after(kKMgNorm, s, (x_check == rhs ? 8.0 : 16.0) * n);
@@ -554,7 +562,9 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   if (!in_out) return CISDC_E_CUDA;  // unreachable with even sweep counts
   // species that met the tolerance at x = b never had a sweep write `out`
   const dim3 cg((unsigned)std::min<long long>((g.ncell + 255) / 256, 4096), (unsigned)g.S, 1);
+  hook->before(kKMgNorm, s);
   k_mg_copy_unswept<<<cg, 256, 0, s>>>(rhs, out, g.ncell, h.d_cycles);
+  hook->after(kKMgNorm, s, 0.0);
   if (cudaGetLastError() != cudaSuccess) return CISDC_E_CUDA;
   return CISDC_OK;
 }

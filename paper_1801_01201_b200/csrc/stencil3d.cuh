@@ -17,20 +17,24 @@
 
 namespace cisdc_b200 {
 
-constexpr int kTX = 32, kTY = 8, kHalo = 2, kRows = 2;
+#ifndef CISDC_TILE_ROWS
+#define CISDC_TILE_ROWS 1
+#endif
+constexpr int kTX = 32, kTY = 8, kHalo = 2, kRows = CISDC_TILE_ROWS;
 constexpr int kTileW = kTX + 2 * kHalo, kTileH = kTY * kRows + 2 * kHalo;
-constexpr int kTileN = kTileW * kTileH;                           // 720
-constexpr int kTilePer = (kTileN + kTX * kTY - 1) / (kTX * kTY);  // 3 elements per thread
+constexpr int kTileN = kTileW * kTileH;                           // 432
+constexpr int kTilePer = (kTileN + kTX * kTY - 1) / (kTX * kTY);  // 2 elements per thread
 
 __device__ __forceinline__ int wrap_any(int x, int n) {
   x %= n;
   return x < 0 ? x + n : x;
 }
 
-// The tile elements this thread stages: smem slot and in-plane global offset.
+// The tile elements this thread stages: smem slot and in-plane offset (32-bit: one species' field
+// is < 2^32 cells, checked by the launcher).  Only the last element can fall outside the tile.
 struct TileLoader {
   int slot[kTilePer];
-  long long off[kTilePer];
+  unsigned off[kTilePer];
   __device__ __forceinline__ void init(int nx, int ny, int i0, int j0) {
     const int t = threadIdx.y * kTX + threadIdx.x;
 #pragma unroll
@@ -39,21 +43,22 @@ struct TileLoader {
       if (idx < kTileN) {
         const int r = idx / kTileW, c = idx - r * kTileW;
         slot[u] = r * (kTileW + 1) + c;
-        off[u] = (long long)wrap_any(j0 + r - kHalo, ny) * nx + wrap_any(i0 + c - kHalo, nx);
+        off[u] = (unsigned)wrap_any(j0 + r - kHalo, ny) * (unsigned)nx + (unsigned)wrap_any(i0 + c - kHalo, nx);
       } else {
         slot[u] = -1;
         off[u] = 0;
       }
     }
   }
+  __device__ __forceinline__ static bool full(int u) { return (u + 1) * kTX * kTY <= kTileN; }
   __device__ __forceinline__ void fetch(const double* __restrict__ plane, double (&v)[kTilePer]) const {
 #pragma unroll
-    for (int u = 0; u < kTilePer; ++u) v[u] = slot[u] >= 0 ? __ldg(plane + off[u]) : 0.0;
+    for (int u = 0; u < kTilePer; ++u) v[u] = (full(u) || slot[u] >= 0) ? __ldg(plane + off[u]) : 0.0;
   }
   __device__ __forceinline__ void store(double* tile, const double (&v)[kTilePer]) const {
 #pragma unroll
     for (int u = 0; u < kTilePer; ++u)
-      if (slot[u] >= 0) tile[slot[u]] = v[u];
+      if (full(u) || slot[u] >= 0) tile[slot[u]] = v[u];
   }
 };
 
@@ -77,6 +82,8 @@ inline dim3 tile3d_grid(int nx, int ny, int nz, int S) {
   return dim3((unsigned)((nx + kTX - 1) / kTX), (unsigned)((ny + kTY * kRows - 1) / (kTY * kRows)),
               (unsigned)(S * ((nz + kZChunk - 1) / kZChunk)));
 }
+// the tiled kernels index one species' field with 32-bit offsets
+inline bool tile3d_ok(long long ncell) { return ncell < (1LL << 32); }
 #endif
 
 using TileArr = double[kTileH][kTileW + 1];
@@ -85,71 +92,100 @@ using TileArr = double[kTileH][kTileW + 1];
 // slower (C5: F_A/F_D 1.6 -> 2.0 ms per launch at 3 blocks)
 constexpr int kEvalMinBlocks = 1, kMgMinBlocks = 1;
 
-// Walks the z-chunk of one species stack f; for every in-range point calls
-// body(r, k, cell, v, aux) (r = the thread's row slot) with the 3 x 5 taps v[axis][offset + 2] of plane k and aux[cell]
-// (aux may be null: then 0).
-template <class Body>
+// hides a pointer's provenance from the optimiser so that `p + 32-bit offset` stays a single
+// wide multiply-add instead of being re-associated into 64-bit index arithmetic
+template <class T>
+__device__ __forceinline__ T* opaque(T* p) {
+  asm("" : "+l"(p));
+  return p;
+}
+
+template <int P>
+struct Phase {
+  static constexpr int value = P;
+};
+
+// Walks the z-chunk of one species field f (and the matching auxiliary field aux, may be null);
+// for every plane k calls plane(k) once, then for every point of the thread's rows
+// body(r, k, cell, v, aux, ok) (r = the thread's row slot, cell = in-field offset, ok = the point
+// is inside the grid: rows past the edge run on clamped data and must not write) with the 3 x 5
+// taps v[axis][offset + 2] and aux[cell] (0 without aux).
+//
+// The z taps live in a 5-deep register queue per row.  The plane loop is unrolled by 5 with the
+// queue phase a compile-time constant, so the queue "rotates" by renaming instead of register
+// moves.  All addressing is 32-bit inside the species field.
+template <class PlaneFn, class Body>
 __device__ __forceinline__ void walk_tiled(const double* __restrict__ f, const double* __restrict__ aux, int nx,
-                                           int ny, int nz, const ZChunk& z, TileArr& tile, Body body) {
+                                           int ny, int nz, const ZChunk& z, TileArr& tile, PlaneFn plane,
+                                           Body body) {
   const int i0 = blockIdx.x * kTX, j0 = blockIdx.y * kTY * kRows;
   const int i = i0 + threadIdx.x;
-  const long long pl = (long long)nx * ny;
+  const unsigned pl = (unsigned)nx * (unsigned)ny;
+  f = opaque(f);
+  if (aux) aux = opaque(aux);
   bool in[kRows];
-  int jr[kRows];
-  long long col[kRows];
+  unsigned col[kRows];
   double q[kRows][5], a_nx[kRows];
 #pragma unroll
   for (int r = 0; r < kRows; ++r) {
-    jr[r] = j0 + threadIdx.y + r * kTY;
-    in[r] = i < nx && jr[r] < ny;
-    col[r] = (long long)(in[r] ? jr[r] : 0) * nx + (in[r] ? i : 0);
-    q[r][0] = __ldg(f + wrapi(z.k0 - 2, nz) * pl + col[r]);
-    q[r][1] = __ldg(f + wrapi(z.k0 - 1, nz) * pl + col[r]);
-    q[r][2] = __ldg(f + (long long)z.k0 * pl + col[r]);
-    q[r][3] = __ldg(f + wrapi(z.k0 + 1, nz) * pl + col[r]);
-    q[r][4] = __ldg(f + wrapi(z.k0 + 2, nz) * pl + col[r]);
-    a_nx[r] = aux ? __ldg(aux + (long long)z.k0 * pl + col[r]) : 0.0;
+    const int jr = j0 + threadIdx.y + r * kTY;
+    in[r] = i < nx && jr < ny;
+    col[r] = in[r] ? (unsigned)jr * (unsigned)nx + (unsigned)i : 0u;
+#pragma unroll
+    for (int o = 0; o < 5; ++o) q[r][o] = __ldg(f + (unsigned)wrapi(z.k0 + o - 2, nz) * pl + col[r]);
+    a_nx[r] = aux ? __ldg(aux + (unsigned)z.k0 * pl + col[r]) : 0.0;
   }
   TileLoader L;
   L.init(nx, ny, i0, j0);
   double pre[kTilePer];
-  L.fetch(f + (long long)z.k0 * pl, pre);
+  L.fetch(f + (unsigned)z.k0 * pl, pre);
   L.store(&tile[0][0], pre);
   const int tx = threadIdx.x + kHalo;
-  for (int k = z.k0; k < z.k1; ++k) {
+  // planes k-2 .. k+2 sit in q[r][(P + o) % 5]; afterwards slot P (plane k-2) takes plane k+3
+  auto step = [&](auto ph, int k) {
+    constexpr int P = decltype(ph)::value;
     __syncthreads();  // tile(k) complete
     const bool more = k + 1 < z.k1;
+    const unsigned kp = (unsigned)k * pl, kn = kp + pl;
+    const double* f3 = opaque(f + (unsigned)wrapi(k + 3, nz) * pl);
+    const double* fn = opaque(f + kn);
+    const double* an = aux ? opaque(aux + kn) : nullptr;
     double q5[kRows], a_cur[kRows];
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {  // prefetch for plane k+1
       a_cur[r] = a_nx[r];
-      q5[r] = more ? __ldg(f + wrapi(k + 3, nz) * pl + col[r]) : 0.0;
-      if (aux && more) a_nx[r] = __ldg(aux + (long long)(k + 1) * pl + col[r]);
+      q5[r] = more ? __ldg(f3 + col[r]) : 0.0;
+      if (aux && more) a_nx[r] = __ldg(an + col[r]);
     }
-    if (more) L.fetch(f + (long long)(k + 1) * pl, pre);
+    if (more) L.fetch(fn, pre);
+    plane(k);
 #pragma unroll
     for (int r = 0; r < kRows; ++r) {
-      if (!in[r]) continue;
       const int ty = threadIdx.y + r * kTY + kHalo;
       double v[3][5];
 #pragma unroll
-      for (int o2 = 0; o2 < 5; ++o2) {
-        v[0][o2] = tile[ty][tx + o2 - 2];
-        v[1][o2] = tile[ty + o2 - 2][tx];
-        v[2][o2] = q[r][o2];
+      for (int o = 0; o < 5; ++o) {
+        v[0][o] = tile[ty][tx + o - 2];
+        v[1][o] = o == 2 ? v[0][2] : tile[ty + o - 2][tx];
+        v[2][o] = q[r][(P + o) % 5];
       }
-      body(r, k, (long long)k * pl + col[r], v, a_cur[r]);
+      body(r, k, kp + col[r], v, a_cur[r], in[r]);
     }
     __syncthreads();  // everyone is done with tile(k)
     if (more) L.store(&tile[0][0], pre);
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      q[r][0] = q[r][1];
-      q[r][1] = q[r][2];
-      q[r][2] = q[r][3];
-      q[r][3] = q[r][4];
-      q[r][4] = q5[r];
-    }
+    for (int r = 0; r < kRows; ++r) q[r][P] = q5[r];
+  };
+  for (int k = z.k0; k < z.k1; k += 5) {
+    step(Phase<0>{}, k);
+    if (k + 1 >= z.k1) break;
+    step(Phase<1>{}, k + 1);
+    if (k + 2 >= z.k1) break;
+    step(Phase<2>{}, k + 2);
+    if (k + 3 >= z.k1) break;
+    step(Phase<3>{}, k + 3);
+    if (k + 4 >= z.k1) break;
+    step(Phase<4>{}, k + 4);
   }
 }
 
@@ -159,11 +195,13 @@ __global__ void __launch_bounds__(kTX* kTY, kEvalMinBlocks) k_eval_ad3_tiled(Ops
                                                               int kc) {
   __shared__ TileArr tile;
   const ZChunk z = zchunk(g.nz, kc);
-  const double* f = phi + (long long)z.s * g.ncell;
   const long long sbase = (long long)z.s * g.ncell;
+  const double* f = phi + sbase;
+  double* fas = fa ? opaque(fa + sbase) : nullptr;
+  double* fds = fd ? opaque(fd + sbase) : nullptr;
   const int s = z.s;
   // Face velocities u_a = (T_a0[i] T_a1[j]) T_a2[k] (face_u): the (i, j) factors of the right and
-  // left faces are formed once per thread-row, times T_a2 per plane (same bits as face_u).
+  // left faces are formed once per thread-row, times T_a2 once per plane (same bits as face_u).
   const int ic = min(blockIdx.x * kTX + threadIdx.x, g.nx - 1);
   double pr[kRows][3], pl[kRows][3];
   const double* t2[3];
@@ -185,29 +223,48 @@ __global__ void __launch_bounds__(kTX* kTY, kEvalMinBlocks) k_eval_ad3_tiled(Ops
       pl[r][a] = (t0 ? __ldg(t0 + il) : 1.0) * (t1 ? __ldg(t1 + jl) : 1.0);
     }
   }
-  walk_tiled(f, nullptr, g.nx, g.ny, g.nz, z, tile,
-             [&](int r, int k, long long cell, const double (&v)[3][5], double) {
-               const long long e = sbase + cell;
-               if (fa) {
-                 double acc = 0.0;
+  double t2r[3], t2l[3];
+  // z faces: the right-face flux of plane k is the left-face flux of plane k+1 in the same column
+  // (same velocity bits: for a = 2 pl == pr and T2 index k; same bracket operands), so it is carried
+  double fz_carry[kRows];
+  int carry_k = -1;
+  walk_tiled(
+      f, nullptr, g.nx, g.ny, g.nz, z, tile,
+      [&](int k) {
 #pragma unroll
-                 for (int a = 0; a < 3; ++a) {
-                   if (!adv[a]) continue;
-                   const double ur = pr[r][a] * (t2[a] ? __ldg(t2[a] + k) : 1.0);
-                   const double ul = pl[r][a] * (t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0);
-                   const double fr = ur * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
-                   const double fl = ul * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
-                   acc = acc + (fr - fl) * ca[a];
-                 }
-                 fa[e] = -acc;
-               }
-               if (fd) {
-                 double lap = 0.0;
+        for (int a = 0; a < 3; ++a) {
+          t2r[a] = t2[a] ? __ldg(t2[a] + k) : 1.0;
+          t2l[a] = t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0;
+        }
+      },
+      [&](int r, int k, unsigned cell, const double (&v)[3][5], double, bool ok) {
+        if (fas) {
+          double acc = 0.0;
 #pragma unroll
-                 for (int a = 0; a < 3; ++a) lap = lap + cd[a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
-                 fd[e] = lap;
-               }
-             });
+          for (int a = 0; a < 3; ++a) {
+            if (!adv[a]) continue;
+            const double ur = pr[r][a] * t2r[a];
+            const double fr = ur * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
+            double fl;
+            if (a == 2 && carry_k == k) {
+              fl = fz_carry[r];
+            } else {
+              const double ul = pl[r][a] * t2l[a];
+              fl = ul * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
+            }
+            if (a == 2) fz_carry[r] = fr;
+            acc = acc + (fr - fl) * ca[a];
+          }
+          if (ok) fas[cell] = -acc;
+        }
+        if (fds) {
+          double lap = 0.0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) lap = lap + cd[a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
+          if (ok) fds[cell] = lap;
+        }
+        if (r == kRows - 1) carry_k = k + 1;
+      });
 }
 
 }  // namespace cisdc_b200
