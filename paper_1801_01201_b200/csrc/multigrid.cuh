@@ -212,7 +212,8 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
                                                          const double* __restrict__ b, double* __restrict__ xo,
                                                          int nx, int ny, int nz, int kc, const int* __restrict__ active,
                                                          double* __restrict__ out, double* __restrict__ bmax) {
-  __shared__ TileArr tile;
+  __shared__ TileRing ring;
+  __shared__ AuxRing aring;
   __shared__ double red[kTX * kTY / 32];
   __shared__ double redb[kTX * kTY / 32];
   const ZChunk z = zchunk(nz, kc);
@@ -223,21 +224,21 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_tiled(x + sbase, b + sbase, nx, ny, nz, z, tile, [](int) {},
-             [&](int, int, unsigned cell, const double (&v)[3][5], double bv, bool ok) {
-               // mg_ax_taps with the species coefficients hoisted (same expression)
-               double lap = 0.0;
-               lap = lap + cs0 * (-v[0][0] + 16.0 * v[0][1] - 30.0 * v[0][2] + 16.0 * v[0][3] - v[0][4]);
-               lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
-               lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
-               const double r = bv - (v[0][2] - coef * lap);
-               if (MODE == 0) {
-                 if (ok) xos[cell] = v[2][2] + wd * r;
-               } else if (ok) {
-                 m = max_keep(m, fabs(r));
-                 if (MODE == 2) mb = max_keep(mb, fabs(bv));
-               }
-             });
+  walk_tiled<true>(x + sbase, b + sbase, nx, ny, nz, z, ring, &aring, [](int) {},
+                   [&](int, unsigned cell, const double (&v)[3][5], double bv, bool ok) {
+                     // mg_ax_taps with the species coefficients hoisted (same expression)
+                     double lap = 0.0;
+                     lap = lap + cs0 * (-v[0][0] + 16.0 * v[0][1] - 30.0 * v[0][2] + 16.0 * v[0][3] - v[0][4]);
+                     lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
+                     lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
+                     const double r = bv - (v[0][2] - coef * lap);
+                     if (MODE == 0) {
+                       if (ok) __stcg(xos + cell, v[2][2] + wd * r);
+                     } else if (ok) {
+                       m = max_keep(m, fabs(r));
+                       if (MODE == 2) mb = max_keep(mb, fabs(bv));
+                     }
+                   });
   if (MODE >= 1) {
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
