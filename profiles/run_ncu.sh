@@ -1,0 +1,27 @@
+#!/bin/bash
+# ncu recipe for the profiles/ summaries (run on the GPU box from the repo root, one GPU):
+#   bash profiles/run_ncu.sh <tag> [config] [scale]
+# 1. launch list (serialised per-launch durations) of one SDC step through the C-ABI
+# 2. --set full captures of the hot kernels, exported on the box to CSV (raw metrics, details,
+#    source) so that only small files travel back
+set -x
+TAG=${1:-r1}
+CFG=${2:-c5}
+SCALE=${3:-1}
+N=/usr/local/cuda/bin/ncu
+mkdir -p gpurun_out
+STEP="python tests/profile_step.py --config $CFG --scale $SCALE"
+$N --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv $STEP > gpurun_out/ncu_${TAG}_l.log 2>&1
+cap() {  # name regex count
+  local rep=/tmp/${TAG}_${CFG}_$1
+  $N --set full --clock-control none --import-source on -k "regex:$2" -c $3 -f -o $rep $STEP > gpurun_out/ncu_${TAG}_$1.log 2>&1
+  $N -i $rep.ncu-rep --page raw --csv > gpurun_out/${TAG}_${CFG}_$1_raw.csv 2>/dev/null
+  $N -i $rep.ncu-rep --page details --csv > gpurun_out/${TAG}_${CFG}_$1_details.csv 2>/dev/null
+  $N -i $rep.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_${CFG}_$1_source.csv 2>/dev/null
+  gzip -f gpurun_out/${TAG}_${CFG}_$1_source.csv
+}
+cap mg3 k_mg3_tiled 4
+cap eval k_eval_ad3 1
+cap react "k_react<" 2
+cap rhs "k_rhs|k_quad|k_mg_update|copy_unswept" 4
+ls -la gpurun_out

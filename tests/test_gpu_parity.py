@@ -265,3 +265,22 @@ def test_order_of_accuracy_matches_oracle(gpu, oracle):
         assert abs(cg.slope - cc.slope) <= 0.05
         band = 0.25 if cg.sweeps == 2 else 0.4
         assert abs(cg.slope - cg.sweeps) <= band, (cg.scheme, cg.sweeps, cg.slope)
+
+
+# ------------------------------------------------------------------ division by reciprocal (newton.cuh)
+
+def test_div_by_bitexact(gpu, tmp_path):
+    """div_by (one IEEE reciprocal per pivot + two exact-residual corrections) == IEEE a / b, bit for
+    bit, on 3 x 2^26 random, binade-edge and near-midpoint operand pairs."""
+    import os
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    exe = str(tmp_path / "div_check")
+    subprocess.run([nvcc, "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-fmad=false",
+                    "-I", os.path.join(root, "include"), "-I", os.path.join(root, "paper_1801_01201_b200", "csrc"),
+                    os.path.join(root, "tests", "cuda", "div_check.cu"), "-o", exe], check=True, capture_output=True)
+    out = subprocess.run([exe, str(1 << 26)], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
