@@ -203,6 +203,16 @@ double F8(const cisdc_gpu_ctx* c) { return 8.0 * (double)c->g.n; }  // bytes of 
 
 // ---------------------------------------------------------------- kernel launchers
 
+// register budget of the tiled 3-D F_A/F_D kernel: 2 resident blocks (no spills) by default;
+// CISDC_EVAL_MIN_BLOCKS=3 trades a few spills for occupancy (measurement knob)
+int eval_min_blocks() {
+  static const int v = [] {
+    const char* e = std::getenv("CISDC_EVAL_MIN_BLOCKS");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
+}
+
 int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd, cudaStream_t s) {
   const Geom& g = ctx->g;
   const dim3 grid = stencil_grid(g.nx, g.ny, g.nz, g.S, g.ndim), block = stencil_block(g.ndim);
@@ -215,8 +225,12 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
         k_eval_ad<3><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd);
         break;
       }
-      k_eval_ad3_tiled<<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa, fd,
-                                                                                      kZChunk);
+      if (eval_min_blocks() >= 3)
+        k_eval_ad3_tiled<3><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa, fd,
+                                                                                           kZChunk);
+      else
+        k_eval_ad3_tiled<2><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa, fd,
+                                                                                           kZChunk);
       break;
   }
   ctx->tm.after(kKEvalAD, s, F8(ctx) * (1 + (fa != nullptr) + (fd != nullptr)));

@@ -174,22 +174,71 @@ __global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int*
   flag[0] = any;
 }
 
-template <int DIM>
+// max of non-negative values, NaN ignored (the oracle's `if (r > m) m = r`)
+__device__ __forceinline__ double max_keep(double m, double r) { return r > m ? r : m; }
+
+// block max of m (and mb) -> one atomic per block into out[s] (bmax[s]); all threads participate
+template <bool BMAX>
+__device__ __forceinline__ void block_max_atomic(double m, double mb, double* red, double* redb, double* out,
+                                                 double* bmax) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    m = max_keep(m, __shfl_down_sync(0xffffffffu, m, off));
+    if (BMAX) mb = max_keep(mb, __shfl_down_sync(0xffffffffu, mb, off));
+  }
+  const int t = threadIdx.y * blockDim.x + threadIdx.x, nw = (int)(blockDim.x * blockDim.y) / 32;
+  if ((t & 31) == 0) {
+    red[t >> 5] = m;
+    redb[t >> 5] = mb;
+  }
+  __syncthreads();
+  if (t == 0) {
+    for (int w = 1; w < nw; ++w) {
+      m = max_keep(m, red[w]);
+      mb = max_keep(mb, redb[w]);
+    }
+    if (m > 0.0) atomic_max_nonneg(out, m);
+    if (BMAX && mb > 0.0) atomic_max_nonneg(bmax, mb);
+  }
+}
+
+// Weighted Jacobi sweep x -> xo.  NORM: the sweep's residual r = b - A x is also the residual of
+// its INPUT iterate, so ||r||_inf (and ||b||_inf with BMAX) of the input is reduced on the fly:
+// the convergence check of x and the cycle's first sweep from x are one pass (the decision kernel
+// runs after it; a species found converged keeps x, see mg_solve_dim).
+template <int DIM, bool NORM = false, bool BMAX = false>
 __global__ void __launch_bounds__(256) k_mg_smooth(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                    const double* __restrict__ b, double* __restrict__ xo, int nx,
-                                                   int ny, int nz, int from_zero, const int* __restrict__ active) {
+                                                   int ny, int nz, int from_zero, const int* __restrict__ active,
+                                                   double* __restrict__ out = nullptr,
+                                                   double* __restrict__ bmax = nullptr) {
   Pt p;
-  if (!grid_point(nx, ny, nz, p)) return;
-  if (!active[p.s]) return;
+  const bool inr = grid_point(nx, ny, nz, p);
+  if (!active[p.s]) return;  // uniform per block
   const long long ncell = (long long)nx * ny * nz;
   const long long e = (long long)p.s * ncell + p.cell;
-  if (from_zero) {
-    xo[e] = C.wD[p.s] * b[e];
-    return;
+  if (!NORM) {
+    if (!inr) return;
+    if (from_zero) {
+      xo[e] = C.wD[p.s] * b[e];
+      return;
+    }
   }
-  const double* xs = x + (long long)p.s * ncell;
-  const double r = b[e] - mg_ax<DIM>(C, p.s, xs, nx, ny, nz, p.i, p.j, p.k);
-  xo[e] = xs[p.cell] + C.wD[p.s] * r;
+  double m = 0.0, mb = 0.0;
+  if (inr) {
+    const double* xs = x + (long long)p.s * ncell;
+    const double bv = b[e];
+    const double r = bv - mg_ax<DIM>(C, p.s, xs, nx, ny, nz, p.i, p.j, p.k);
+    xo[e] = xs[p.cell] + C.wD[p.s] * r;
+    if (NORM) {
+      m = fabs(r);
+      if (BMAX) mb = fabs(bv);
+    }
+  }
+  if (NORM) {
+    __shared__ double red[8], redb[8];
+    block_max_atomic<BMAX>(m, mb, red, redb, out + p.s, bmax + p.s);
+  }
 }
 
 // 3-D levels: 2.5-D blocked versions (stencil3d.cuh) of the smoother and the residual norm.
@@ -202,12 +251,9 @@ __device__ __forceinline__ double mg_ax_taps(const MgCoef& C, int s, const doubl
   return v[0][2] - C.coef * lap;
 }
 
-// max of non-negative values, NaN ignored (the oracle's `if (r > m) m = r`)
-__device__ __forceinline__ double max_keep(double m, double r) { return r > m ? r : m; }
-
-// mode 0: smooth x -> xo (not from zero); mode 1: residual inf-norm into out[s]; mode 2: also
-// ||b||_inf into bmax[s]
-template <int MODE>
+// SMOOTH: x -> xo (not from zero); NORM: ||b - A x||_inf per species into out[s] (of the input
+// x; fused with SMOOTH this is the check + first sweep of a cycle); BMAX: also ||b||_inf into bmax[s]
+template <bool SMOOTH, bool NORM, bool BMAX>
 __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                          const double* __restrict__ b, double* __restrict__ xo,
                                                          int nx, int ny, int nz, int kc, const int* __restrict__ active,
@@ -220,7 +266,7 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
   if (!active[z.s]) return;  // uniform per block
   const long long ncell = (long long)nx * ny * nz;
   const long long sbase = (long long)z.s * ncell;
-  double* xos = MODE == 0 ? opaque(xo + sbase) : nullptr;
+  double* xos = SMOOTH ? opaque(xo + sbase) : nullptr;
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
@@ -232,34 +278,12 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
                      lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
                      lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
                      const double r = bv - (v[0][2] - coef * lap);
-                     if (MODE == 0) {
-                       if (ok) __stcg(xos + cell, v[2][2] + wd * r);
-                     } else if (ok) {
-                       m = max_keep(m, fabs(r));
-                       if (MODE == 2) mb = max_keep(mb, fabs(bv));
-                     }
+                     if (!ok) return;
+                     if (SMOOTH) __stcg(xos + cell, v[2][2] + wd * r);
+                     if (NORM) m = max_keep(m, fabs(r));
+                     if (BMAX) mb = max_keep(mb, fabs(bv));
                    });
-  if (MODE >= 1) {
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      m = max_keep(m, __shfl_down_sync(0xffffffffu, m, off));
-      if (MODE == 2) mb = max_keep(mb, __shfl_down_sync(0xffffffffu, mb, off));
-    }
-    const int t = threadIdx.y * kTX + threadIdx.x;
-    if ((t & 31) == 0) {
-      red[t >> 5] = m;
-      redb[t >> 5] = mb;
-    }
-    __syncthreads();
-    if (t == 0) {
-      for (int w = 1; w < kTX * kTY / 32; ++w) {
-        m = max_keep(m, red[w]);
-        mb = max_keep(mb, redb[w]);
-      }
-      if (m > 0.0) atomic_max_nonneg(out + z.s, m);
-      if (MODE == 2 && mb > 0.0) atomic_max_nonneg(bmax + z.s, mb);
-    }
-  }
+  if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
 }
 
 // launched on the COARSE grid
@@ -434,24 +458,56 @@ struct MgRunner {
   // every pair of sweeps .x holds the iterate again for active AND masked (converged) species.
   const double* b0;
   const double* first_x = nullptr;  // the initial iterate x = b is read straight from the rhs
+  bool check_next = false;          // the next level-0 sweep also reduces the residual norm of its input
+  bool first_check = true;          // ... and ||b||_inf (the first check of the solve)
+  DevStatus* st = nullptr;
 
   const double* bof(int l) const { return l == 0 ? b0 : h.lv[l].b; }
   dim3 grid(const MgLevel& Lv) const { return stencil_grid(Lv.nx, Lv.ny, Lv.nz, h.S, DIM); }
   dim3 block() const { return stencil_block(DIM); }
 
+  // per-species decision of the oracle's loop on the reduced norms (enables the rest of the cycle)
+  void update() {
+    hook->before(kKMgNorm, s);
+    k_mg_update<<<1, 32, 0, s>>>(h.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
+                                 h.d_flag, st);
+    hook->after(kKMgNorm, s, 0.0);
+  }
+
   void smooth(int l, bool from_zero) {
     MgLevel& Lv = h.lv[l];
     const double* xin = (l == 0 && first_x) ? first_x : Lv.x;
     if (l == 0) first_x = nullptr;
-    hook->before(kKMgSmooth, s);
-    if (DIM == 3 && !from_zero && tile3d_ok(Lv.ncell))
-      k_mg3_tiled<0><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
+    const bool chk = l == 0 && check_next;
+    const bool bm = chk && first_check;
+    const bool tiled = DIM == 3 && !from_zero && tile3d_ok(Lv.ncell);
+    const double n8 = 8.0 * Lv.ncell * h.S;
+    hook->before(chk ? kKMgNorm : kKMgSmooth, s);
+    if (tiled && bm)
+      k_mg3_tiled<true, true, true><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
+          C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, h.d_rmax, h.d_bmax);
+    else if (tiled && chk)
+      k_mg3_tiled<true, true, false><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
+          C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, h.d_rmax, nullptr);
+    else if (tiled)
+      k_mg3_tiled<true, false, false><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
           C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, nullptr, nullptr);
+    else if (bm)
+      k_mg_smooth<DIM, true, true><<<grid(Lv), block(), 0, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, 0,
+                                                                 h.d_active, h.d_rmax, h.d_bmax);
+    else if (chk)
+      k_mg_smooth<DIM, true, false><<<grid(Lv), block(), 0, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, 0,
+                                                                  h.d_active, h.d_rmax, nullptr);
     else
       k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
                                                     h.d_active);
-    hook->after(kKMgSmooth, s, 8.0 * Lv.ncell * h.S * (from_zero ? 2 : 3));
+    hook->after(chk ? kKMgNorm : kKMgSmooth, s, n8 * (from_zero ? 2 : 3));
     std::swap(Lv.x, Lv.t);
+    if (chk) {
+      check_next = false;
+      first_check = false;
+      update();
+    }
   }
   void vcycle(int l) {
     MgLevel& Lv = h.lv[l];
@@ -474,6 +530,15 @@ struct MgRunner {
   }
 };
 
+// The oracle's loop per species: x = b; while (||b - A x|| > tol ||b||) { cap check; V-cycle }.
+// Device form: every enqueued V-cycle starts with a level-0 sweep that also reduces the residual
+// norm of its input iterate (k_mg3_tiled<.., NORM> / k_mg_smooth<.., NORM>), followed by the
+// decision kernel; a species found converged is masked out for the rest of the cycle and keeps
+// its iterate (the sweep wrote the ping-pong partner, which an even sweep count never hands back).
+// So n real cycles cost n + 1 enqueued cycles, the last one a masked no-op after its first sweep.
+// The host enqueues cycles in batches (predicted from the last solve with this coefficient) and
+// only then reads the device flag.  Without a level-0 pre-sweep (mg_pre == 0) the check is a
+// separate residual-norm pass.
 template <int DIM>
 inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
                         double* out, DevStatus* st, cudaStream_t s, LaunchHook* hook) {
@@ -483,6 +548,7 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     return CISDC_OK;
   }
   MgRunner<DIM> R{h, d, {}, 1, s, hook, rhs};
+  R.st = st;
   R.L = mg_plan(h, d, coef, R.C);
   std::vector<int> ones(g.S, 1);
   cudaMemcpyAsync(h.d_active, ones.data(), sizeof(int) * g.S, cudaMemcpyHostToDevice, s);
@@ -498,64 +564,72 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   double* own_t = L0.t;
   L0.x = out;
   R.first_x = rhs;
-  const double* x_check = rhs;  // the first check sees x = b (and also forms ||b||_inf)
-  // The host enqueues cycles in batches (predicted from the last solve with this coefficient) and
-  // only then looks at the device flag: cycles past convergence are masked no-ops, so the result
-  // is identical to checking after every cycle.
-  int batch = 1;
-  for (const auto& pc : h.predicted)
-    if (pc.first == coef) batch = std::max(1, pc.second);
-  // check = residual norm + per-species decision (the decision enables the next V-cycle)
+  const bool fused = d.mg_pre >= 1;
+  const double* x_check = rhs;  // separate-check path: the first check sees x = b
   auto check = [&]() {
     hook->before(kKMgNorm, s);
     const dim3 rb = R.block();
     const dim3 rg((L0.nx + rb.x - 1) / rb.x, (L0.ny + rb.y - 1) / rb.y, g.S);
     double* bmax = x_check == rhs ? h.d_bmax : nullptr;
     if (DIM == 3 && tile3d_ok(L0.ncell) && bmax)
-      k_mg3_tiled<2><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
+      k_mg3_tiled<false, true, true><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
           R.C[0], x_check, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax, bmax);
     else if (DIM == 3 && tile3d_ok(L0.ncell))
-      k_mg3_tiled<1><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
+      k_mg3_tiled<false, true, false><<<tile3d_grid(L0.nx, L0.ny, L0.nz, g.S), dim3(kTX, kTY), 0, s>>>(
           R.C[0], x_check, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax, nullptr);
     else
       k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], x_check, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax, bmax);
     hook->after(kKMgNorm, s, (x_check == rhs ? 8.0 : 16.0) * n);
     x_check = L0.x;
-    hook->before(kKMgNorm, s);
-    k_mg_update<<<1, 32, 0, s>>>(g.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
-                                 h.d_flag, st);
-    hook->after(kKMgNorm, s, 0.0);
+    R.update();
   };
-  check();
-  int launched = 0;
-  for (;;) {
-    for (int b = 0; b < batch && launched < d.mg_max_cycles; ++b, ++launched) {
-      R.vcycle(0);
-      check();
+  int batch = 1;
+  for (const auto& pc : h.predicted)
+    if (pc.first == coef) batch = std::max(1, pc.second);
+  int launched = 0;  // V-cycles enqueued
+  if (fused) {
+    // cycle i checks x_{i-1} first: n real cycles need n + 1 enqueued ones
+    batch += 1;
+    for (;;) {
+      for (int b = 0; b < batch && launched <= d.mg_max_cycles; ++b, ++launched) {
+        R.check_next = true;
+        R.vcycle(0);
+      }
+      cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
+      if (!h.h_flag[0] || h.h_flag[1] || launched > d.mg_max_cycles) break;
+      batch = 1;
     }
-    cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
-    if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
-    if (!h.h_flag[0] || h.h_flag[1] || launched >= d.mg_max_cycles) break;
-    batch = 1;
+  } else {
+    check();
+    for (;;) {
+      for (int b = 0; b < batch && launched < d.mg_max_cycles; ++b, ++launched) {
+        R.vcycle(0);
+        check();
+      }
+      cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
+      if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
+      if (!h.h_flag[0] || h.h_flag[1] || launched >= d.mg_max_cycles) break;
+      batch = 1;
+    }
   }
   // remember how many cycles this coefficient needed (flag[0] == 0 after the last check)
-  int used = launched;
   {
     std::vector<int> cyc(g.S);
     cudaMemcpy(cyc.data(), h.d_cycles, sizeof(int) * g.S, cudaMemcpyDeviceToHost);
-    used = 0;
+    int used = 0;
     for (int v : cyc) used = std::max(used, v);
     used = std::max(used, 1);
-  }
-  bool found = false;
-  for (auto& pc : h.predicted)
-    if (pc.first == coef) {
-      pc.second = used;
-      found = true;
+    bool found = false;
+    for (auto& pc : h.predicted)
+      if (pc.first == coef) {
+        pc.second = used;
+        found = true;
+      }
+    if (!found) {
+      if (h.predicted.size() >= 64) h.predicted.erase(h.predicted.begin());
+      h.predicted.push_back({coef, used});
     }
-  if (!found) {
-    if (h.predicted.size() >= 64) h.predicted.erase(h.predicted.begin());
-    h.predicted.push_back({coef, used});
   }
   const bool in_out = L0.x == out;
   L0.x = own_x;

@@ -102,7 +102,7 @@ struct AuxRing {
   double a[kRing][kTX * kTY];  // 16 KB
 };
 
-constexpr int kEvalMinBlocks = 1, kMgMinBlocks = 1;
+constexpr int kMgMinBlocks = 3;
 
 template <int P>
 struct Phase {
@@ -186,8 +186,9 @@ __device__ __forceinline__ void walk_tiled(const double* __restrict__ f, const d
   cp_async_wait<0>();  // no copy may be outstanding when the block exits
 }
 
-// F_A and/or F_D, 3-D periodic
-__global__ void __launch_bounds__(kTX* kTY, kEvalMinBlocks) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
+// F_A and/or F_D, 3-D periodic; MINB = resident blocks per SM the registers are budgeted for
+template <int MINB>
+__global__ void __launch_bounds__(kTX* kTY, MINB) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
                                                               double* __restrict__ fa, double* __restrict__ fd,
                                                               int kc) {
   __shared__ TileRing ring;

@@ -22,6 +22,6 @@ cap() {  # name regex count
 }
 cap mg3 k_mg3_tiled 4
 cap eval k_eval_ad3 1
-cap react "k_react<" 2
+cap react "^k_react$" 2
 cap rhs "k_rhs|k_quad|k_mg_update|copy_unswept" 4
 ls -la gpurun_out
