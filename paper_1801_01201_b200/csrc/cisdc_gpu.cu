@@ -143,6 +143,7 @@ struct cisdc_gpu_ctx {
   int incr_slot = 0;
   unsigned long long newton_seen = 0, mg_seen = 0;
   cudaStream_t s_main = nullptr, s_r = nullptr;
+  int num_sms = 148;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t ev_base = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
   Timing tm;
@@ -324,6 +325,16 @@ void launch_fixup_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   }
 }
 
+// blocks per SM of the persistent work-queue Newton kernel (0 = one thread per cell);
+// CISDC_REACT_QUEUE_BLOCKS overrides (measurement knob)
+int react_queue_blocks() {
+  static const int v = [] {
+    const char* e = std::getenv("CISDC_REACT_QUEUE_BLOCKS");
+    return e ? std::atoi(e) : rtc_min_blocks();
+  }();
+  return v;
+}
+
 int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t s) {
   if (ctx->rtc.ready) {
     Reaction rx = ctx->rx;
@@ -335,8 +346,16 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t 
     DevStatus* st = ctx->d_st;
     void* args[5] = {&rx, &o, &g, &aa, &st};
     ctx->tm.before(kKReact, s);
-    CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)), dim3(128),
-                        args, 0, s));
+    // per-lane work queue on a persistent grid (default), or one thread per cell
+    const int qb = react_queue_blocks();
+    if (qb > 0) {
+      const long long want = grid_of(ctx->g.ncell, 128);
+      const int blocks = (int)std::min<long long>(want, (long long)qb * ctx->num_sms);
+      CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[4 + mode]), dim3(blocks), dim3(128), args, 0, s));
+    } else {
+      CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)),
+                          dim3(128), args, 0, s));
+    }
     ctx->tm.after(kKReact, s, F8(ctx) * react_fields(mode, a));
     // cells whose LU needed a row interchange: dense generic kernel, then reset the list
     ctx->tm.before(kKReact, s);
@@ -1008,6 +1027,11 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
   TRY(dalloc(ctx, &ctx->d_partial, kIncrBlocks));
   TRY(dalloc(ctx, &ctx->d_incr, kMaxSweepsPerStep));
   CU(cudaMallocHost(&ctx->h_incr, sizeof(double) * kMaxSweepsPerStep));
+  {
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
   CU(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&ctx->s_r, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&ctx->ev_base, cudaEventDisableTiming));
