@@ -226,10 +226,10 @@ def main():
     d_out = torch.empty_like(d_phi0)
     torch.cuda.synchronize()
 
-    # the per-kernel breakdown pass runs the sweeps on one stream (workers <= 1) so that the event
+    # the per-kernel breakdown pass runs the sweeps serially on one stream (workers = 0) so that the event
     # intervals of different kernel classes never overlap
     oc1 = api.IntegrateOptions(scheme=scheme, dt=spec.dt, n_steps=1, M=spec.M, n_sweeps=spec.n_sweeps, nu=spec.nu,
-                               workers=min(workers, 1), convention=spec.convention).to_c()
+                               workers=0, convention=spec.convention).to_c()
 
     def step_device(o=oc):
         ctx.check(lib.cisdc_gpu_integrate_device(ctx.h, C.c_void_p(d_phi0.data_ptr()), n, C.byref(o),
@@ -338,7 +338,7 @@ def main():
             "gpu_launches": launches,
             "roofline": roof,
             "kernels": sorted(classes, key=lambda x: -x["ms"]),
-            "kernels_pass": {"ms_per_step": inst_ms / args.steps, "workers": min(workers, 1),
+            "kernels_pass": {"ms_per_step": inst_ms / args.steps, "workers": 0,
                              "note": "per-kernel CUDA-event pass, same K steps, one stream"},
             "end_to_end_hbm": {"algorithmic_bytes_per_sweep": 8.0 * n * (7 * spec.M + 4),
                                "achieved_gbs": 8.0 * n * (7 * spec.M + 4) * spec.n_sweeps * args.steps / (tmax * 1e-3) / 1e9},

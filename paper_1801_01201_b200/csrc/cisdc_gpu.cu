@@ -226,12 +226,15 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
         k_eval_ad<3><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd);
         break;
       }
-      if (eval_min_blocks() >= 3)
-        k_eval_ad3_tiled<3><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa, fd,
-                                                                                           kZChunk);
+      if (ctx->ops.vconst)
+        k_eval_ad3_tiled<2, true><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa,
+                                                                                                 fd, kZChunk);
+      else if (eval_min_blocks() >= 3)
+        k_eval_ad3_tiled<3, false><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa,
+                                                                                                  fd, kZChunk);
       else
-        k_eval_ad3_tiled<2><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa, fd,
-                                                                                           kZChunk);
+        k_eval_ad3_tiled<2, false><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa,
+                                                                                                  fd, kZChunk);
       break;
   }
   ctx->tm.after(kKEvalAD, s, F8(ctx) * (1 + (fa != nullptr) + (fd != nullptr)));
@@ -325,16 +328,6 @@ void launch_fixup_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   }
 }
 
-// blocks per SM of the persistent work-queue Newton kernel (0 = one thread per cell);
-// CISDC_REACT_QUEUE_BLOCKS overrides (measurement knob)
-int react_queue_blocks() {
-  static const int v = [] {
-    const char* e = std::getenv("CISDC_REACT_QUEUE_BLOCKS");
-    return e ? std::atoi(e) : rtc_min_blocks();
-  }();
-  return v;
-}
-
 int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t s) {
   if (ctx->rtc.ready) {
     Reaction rx = ctx->rx;
@@ -346,16 +339,8 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t 
     DevStatus* st = ctx->d_st;
     void* args[5] = {&rx, &o, &g, &aa, &st};
     ctx->tm.before(kKReact, s);
-    // per-lane work queue on a persistent grid (default), or one thread per cell
-    const int qb = react_queue_blocks();
-    if (qb > 0) {
-      const long long want = grid_of(ctx->g.ncell, 128);
-      const int blocks = (int)std::min<long long>(want, (long long)qb * ctx->num_sms);
-      CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[4 + mode]), dim3(blocks), dim3(128), args, 0, s));
-    } else {
-      CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)),
-                          dim3(128), args, 0, s));
-    }
+    CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)), dim3(128),
+                        args, 0, s));
     ctx->tm.after(kKReact, s, F8(ctx) * react_fields(mode, a));
     // cells whose LU needed a row interchange: dense generic kernel, then reset the list
     ctx->tm.before(kKReact, s);
@@ -951,6 +936,19 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
       }
       o.adv[a] = any;
       if (a < d->ndim) o.cadv[a] = 1.0 / (12.0 * d->h[a]);
+    }
+    // uniform-velocity detection (the tiled 3-D F_A kernel then skips the per-face products)
+    o.vconst = 1;
+    for (int a = 0; a < 3; ++a) {
+      double f[3] = {1.0, 1.0, 1.0};
+      for (int b = 0; b < 3; ++b) {
+        if (!o.vel[a][b]) continue;
+        const double* t = d->vel[a][b];
+        for (int i = 1; i < nn[b]; ++i)
+          if (t[i] != t[0] || std::signbit(t[i]) != std::signbit(t[0])) o.vconst = 0;
+        f[b] = t[0];
+      }
+      o.ucon[a] = (f[0] * f[1]) * f[2];
     }
     for (int s = 0; s < S; ++s) {
       const double ds = d->diffusivity ? d->diffusivity[s] : 0.0;

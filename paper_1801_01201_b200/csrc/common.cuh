@@ -43,6 +43,10 @@ struct Ops {
   int adv[3];               // axis a advects
   double cadv[3];           // 1 / (12 h_a)
   double cdiff[kMaxS][3];   // d_s / (12 h_a^2)
+  // uniform face velocities: every table of every advecting axis is constant (or absent), and
+  // ucon[a] = (T_a0 T_a1) T_a2 -- the per-face product face_u forms, same bits
+  int vconst;
+  double ucon[3];
   // reference Dirichlet problem (CISDC_PROBLEM_REFERENCE_RD)
   int ref_rd;
   double rd_cadv, rd_cdiff, rd_w[2][5];

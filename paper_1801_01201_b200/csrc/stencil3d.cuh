@@ -186,8 +186,9 @@ __device__ __forceinline__ void walk_tiled(const double* __restrict__ f, const d
   cp_async_wait<0>();  // no copy may be outstanding when the block exits
 }
 
-// F_A and/or F_D, 3-D periodic; MINB = resident blocks per SM the registers are budgeted for
-template <int MINB>
+// F_A and/or F_D, 3-D periodic; MINB = resident blocks per SM the registers are budgeted for;
+// UCONST: uniform face velocities (Ops::vconst), u_a = Ops::ucon[a] on every face
+template <int MINB, bool UCONST>
 __global__ void __launch_bounds__(kTX* kTY, MINB) k_eval_ad3_tiled(Ops o, Geom g, const double* __restrict__ phi,
                                                               double* __restrict__ fa, double* __restrict__ fd,
                                                               int kc) {
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(kTX* kTY, MINB) k_eval_ad3_tiled(Ops o, Geom g
     cd[a] = o.cdiff[s][a];
     ca[a] = o.cadv[a];
     t2[a] = o.vel[a][2];
+    if (UCONST) continue;
     const double* t0 = o.vel[a][0];
     const double* t1 = o.vel[a][1];
     const int il = a == 0 ? wrapi(ic - 1, g.nx) : ic, jl = a == 1 ? wrapi(jc - 1, g.ny) : jc;
@@ -226,6 +228,7 @@ __global__ void __launch_bounds__(kTX* kTY, MINB) k_eval_ad3_tiled(Ops o, Geom g
   walk_tiled<false>(
       f, nullptr, g.nx, g.ny, g.nz, z, ring, nullptr,
       [&](int k) {
+        if (UCONST) return;
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
           t2r[a] = t2[a] ? __ldg(t2[a] + k) : 1.0;
@@ -238,13 +241,13 @@ __global__ void __launch_bounds__(kTX* kTY, MINB) k_eval_ad3_tiled(Ops o, Geom g
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             if (!adv[a]) continue;
-            const double ur = pr[a] * t2r[a];
+            const double ur = UCONST ? o.ucon[a] : pr[a] * t2r[a];
             const double fr = ur * (7.0 * (v[a][2] + v[a][3]) - (v[a][1] + v[a][4]));
             double fl;
             if (a == 2 && carry_k == k) {
               fl = fz_carry;
             } else {
-              const double ul = pl[a] * t2l[a];
+              const double ul = UCONST ? o.ucon[a] : pl[a] * t2l[a];
               fl = ul * (7.0 * (v[a][1] + v[a][2]) - (v[a][0] + v[a][3]));
             }
             if (a == 2) fz_carry = fr;

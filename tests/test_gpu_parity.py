@@ -267,20 +267,35 @@ def test_order_of_accuracy_matches_oracle(gpu, oracle):
         assert abs(cg.slope - cg.sweeps) <= band, (cg.scheme, cg.sweeps, cg.slope)
 
 
-# ------------------------------------------------------------------ division by reciprocal (newton.cuh)
+# ------------------------------------------------------------------ 3-D tiled stencils: ragged grids, variable velocity
 
-def test_div_by_bitexact(gpu, tmp_path):
-    """div_by (one IEEE reciprocal per pivot + two exact-residual corrections) == IEEE a / b, bit for
-    bit, on 3 x 2^26 random, binade-edge and near-midpoint operand pairs."""
-    import os
-    import shutil
-    import subprocess
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
-    exe = str(tmp_path / "div_check")
-    subprocess.run([nvcc, "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-fmad=false",
-                    "-I", os.path.join(root, "include"), "-I", os.path.join(root, "paper_1801_01201_b200", "csrc"),
-                    os.path.join(root, "tests", "cuda", "div_check.cu"), "-o", exe], check=True, capture_output=True)
-    out = subprocess.run([exe, str(1 << 26)], capture_output=True, text=True, timeout=300)
-    print(out.stdout)
-    assert out.returncode == 0, out.stdout + out.stderr
+def c5_like(n, vel, seed=11):
+    """The C5 network on an arbitrary 3-D grid (ragged against the 32 x 8 tiles and the 32-plane
+    z-chunks) with the given separable face-velocity tables."""
+    reac, prod, k, D = P._c45_network()
+    p = P.ProblemDesc(ndim=3, n=n, nspecies=9, h=tuple(1.0 / x for x in n), vel=vel, diffusivity=D,
+                      reaction_kind=_abi.REACTION_MASS_ACTION, reactants=reac, products=prod, rate_constants=k,
+                      name="c5-like")
+    P.mg_defaults(p, 1e-10)
+    rng = np.random.default_rng(seed)
+    fields = P._normalised_fields(rng, n, 9, 16, 3)
+    return P.RunSpec(p, P.to_layout(fields), 2, 6, 4, 1e-5, 1, nu=1, name="c5-like", schemes=(2,))
+
+
+def random_velocity_tables(n, seed=3):
+    rng = np.random.default_rng(seed)
+    return {(a, b): rng.uniform(0.2, 1.5, n[b]) * (1 if (a + b) % 2 else -1) for a in range(3) for b in range(3)
+            if (a + b) % 3 != 1}
+
+
+@pytest.mark.parametrize("n,variable", [((40, 20, 36), True), ((40, 20, 36), False), ((16, 8, 70), True),
+                                         ((64, 24, 33), False)])
+def test_tiled_3d_ragged_and_variable_velocity(gpu, oracle, n, variable):
+    """The tiled 3-D F_A/F_D and multigrid kernels (cp.async plane ring, z carry, uniform-velocity
+    specialisation) on grids that are not multiples of the 32 x 8 tile or the 32-plane chunk, with
+    spatially varying (general path) or uniform (specialised path) face velocities: bitwise."""
+    vel = random_velocity_tables(n) if variable else P.constant_velocity_tables((1.0, -0.5, 0.25), n)
+    spec = c5_like(n, vel)
+    for workers in (0, 2):
+        _, g, c = per_step_compare(oracle, spec, 2, 1, workers=workers)
+        assert np.array_equal(g, c)
