@@ -1030,8 +1030,16 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     CU(cudaGetDevice(&dev));
     CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  CU(cudaStreamCreateWithFlags(&ctx->s_main, cudaStreamNonBlocking));
-  CU(cudaStreamCreateWithFlags(&ctx->s_r, cudaStreamNonBlocking));
+  // PMISDC: the D chain (s_main: rhs, multigrid, F_A/F_D) is the critical path; the R chain (s_r:
+  // Newton) fills what it leaves, so s_main gets the higher priority (CISDC_STREAM_PRIO=0 disables)
+  {
+    int lo = 0, hi = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    const char* e = std::getenv("CISDC_STREAM_PRIO");  // 0 none, 1 D chain first, 2 R chain first
+    const int mode = e ? std::atoi(e) : 1;
+    CU(cudaStreamCreateWithPriority(&ctx->s_main, cudaStreamNonBlocking, mode == 1 ? hi : lo));
+    CU(cudaStreamCreateWithPriority(&ctx->s_r, cudaStreamNonBlocking, mode == 2 ? hi : lo));
+  }
   CU(cudaEventCreateWithFlags(&ctx->ev_base, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
   CU(cudaEventCreate(&ctx->ev_t0));
