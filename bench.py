@@ -316,10 +316,25 @@ def main():
         achieved = dom["gbs"]
         roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "peak_source": hbm_src, "traffic": None}
+    # per-class rooflines (HBM classes against the measured copy bandwidth) and the committed ncu
+    # capture of each class (DRAM bytes per launch, FP64 pipe utilisation)
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
+    ncu = {}
     if os.path.exists(prof):
         with open(prof) as f:
-            roof["traffic"] = json.load(f).get(roof["kernel"])
+            ncu = json.load(f)
+    if roof["kernel"] in ncu:
+        roof["traffic"] = ncu[roof["kernel"]].get("dram_bytes")
+        roof["traffic_source"] = ncu[roof["kernel"]].get("source")
+    per_class = []
+    for c in classes:
+        e = {"kernel": c["kernel"], "share": c["share"], "achieved_gbs": c["gbs"], "hbm_frac": (c["gbs"] or 0) / hbm}
+        if c["kernel"] in ncu:
+            e["ncu"] = {k: ncu[c["kernel"]].get(k) for k in ("dram_pct", "fp64_pipe_pct", "l1_pct")}
+        if c["kernel"] == "react_newton" and desc.nspecies >= 9:
+            e["fp64_tflops"] = newton_flops / (c["ms"] * 1e-3) / 1e12
+            e["fp64_frac_dmul_dadd_peak"] = e["fp64_tflops"] / pk_mul.value
+        per_class.append(e)
 
     if rank == 0:
         line = {
@@ -337,6 +352,7 @@ def main():
                     "ms_per_step": e2e_ms / args.steps, "wall_s": wall},
             "gpu_launches": launches,
             "roofline": roof,
+            "rooflines": sorted(per_class, key=lambda x: -x["share"]),
             "kernels": sorted(classes, key=lambda x: -x["ms"]),
             "kernels_pass": {"ms_per_step": inst_ms / args.steps, "workers": 0,
                              "note": "per-kernel CUDA-event pass, same K steps, one stream"},

@@ -128,6 +128,7 @@ struct cisdc_gpu_ctx {
   double* fa_ad[kMaxM + 1] = {};
   double* fd_ad[kMaxM + 1] = {};
   std::vector<double*> slot_bufs;  // (nu-1) * M * 5: phi_ad, phi_r, fa_r, fd_r, fr_r
+  std::vector<double*> diff_bufs;  // CISDCQ rhs difference cache: (M - 3) nodes x {dA, dDR}
   // solvers
   double* rd_work = nullptr;
   MgHierarchy mg;
@@ -377,10 +378,15 @@ int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
     for (int j = 0; j <= a.M; ++j) in.insert(in.end(), {a.sfa[j], a.sfd[j], a.sfr[j]});
   } else {
     in.push_back(a.base);
-    for (int t = 0; t < a.nt; ++t) in.insert(in.end(), {a.t[t].A, a.t[t].Ap, a.t[t].D, a.t[t].Dp, a.t[t].R, a.t[t].Rp});
+    for (int t = 0; t < a.nt; ++t) {
+      if (a.t[t].diff) in.insert(in.end(), {a.t[t].A, a.t[t].D});
+      else in.insert(in.end(), {a.t[t].A, a.t[t].Ap, a.t[t].D, a.t[t].Dp, a.t[t].R, a.t[t].Rp});
+    }
   }
   in.insert(in.end(), {a.X, a.Y, a.Z});
-  const double fields = distinct_fields(in) + 1 + (a.out2 != nullptr) + (a.base_out != nullptr);
+  double outs = 1 + (a.out2 != nullptr) + (a.base_out != nullptr);
+  for (int t = 0; t < a.nt; ++t) outs += a.t[t].outA ? 2 : 0;
+  const double fields = distinct_fields(in) + outs;
   ctx->tm.before(kKRhs, s);
   k_rhs<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(a, ctx->g.n);
   ctx->tm.after(kKRhs, s, F8(ctx) * fields);
@@ -656,6 +662,12 @@ int ensure_slots(cisdc_gpu_ctx* ctx, int nu) {
     TRY(dalloc(ctx, &p, ctx->g.n));
     ctx->slot_bufs.push_back(p);
   }
+  const size_t dneed = ctx->M > 3 ? (size_t)(ctx->M - 3) * 2 : 0;
+  while (ctx->diff_bufs.size() < dneed) {
+    double* p = nullptr;
+    TRY(dalloc(ctx, &p, ctx->g.n));
+    ctx->diff_bufs.push_back(p);
+  }
   return CISDC_OK;
 }
 
@@ -665,16 +677,29 @@ int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt
   RhsArgs r{};
   r.kind = kRhsCisdcq;
   int nt = 0;
+  // the differences of node j's term are read in full by the first row that needs them (m = j+2),
+  // which stores them when rows m+1 .. M will read them again (nodes j <= M-3)
+  const bool cache = (int)ctx->diff_bufs.size() >= 2 * (ctx->M - 3) && ctx->M > 3;
   for (int j = 1; j <= m - 2; ++j) {
     RhsTerm& t = r.t[nt++];
     t.cE = dt * QE(ctx->tb, row, j - 1);
     t.cI = dt * QI(ctx->tb, row, j - 1);
+    if (cache && j < m - 2) {
+      t.diff = 1;
+      t.A = ctx->diff_bufs[2 * (j - 1)];
+      t.D = ctx->diff_bufs[2 * (j - 1) + 1];
+      continue;
+    }
     t.A = W.get(2, j, ell);
     t.Ap = V(ctx, prev, kFa, j);
     t.D = W.get(3, j, ell);
     t.Dp = V(ctx, prev, kFd, j);
     t.R = W.get(4, j, ell);
     t.Rp = V(ctx, prev, kFr, j);
+    if (cache && j <= ctx->M - 3) {
+      t.outA = ctx->diff_bufs[2 * (j - 1)];
+      t.outDR = ctx->diff_bufs[2 * (j - 1) + 1];
+    }
   }
   if (m >= 2) {
     RhsTerm& t = r.t[nt++];

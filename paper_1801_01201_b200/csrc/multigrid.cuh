@@ -482,7 +482,7 @@ struct MgRunner {
     const bool bm = chk && first_check;
     const bool tiled = DIM == 3 && !from_zero && tile3d_ok(Lv.ncell);
     const double n8 = 8.0 * Lv.ncell * h.S;
-    hook->before(chk ? kKMgNorm : kKMgSmooth, s);
+    hook->before(kKMgSmooth, s);  // a checking sweep is still a sweep (its norm is a by-product)
     if (tiled && bm)
       k_mg3_tiled<true, true, true><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
           C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, h.d_rmax, h.d_bmax);
@@ -501,7 +501,7 @@ struct MgRunner {
     else
       k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
                                                     h.d_active);
-    hook->after(chk ? kKMgNorm : kKMgSmooth, s, n8 * (from_zero ? 2 : 3));
+    hook->after(kKMgSmooth, s, n8 * (from_zero ? 2 : 3));
     std::swap(Lv.x, Lv.t);
     if (chk) {
       check_next = false;

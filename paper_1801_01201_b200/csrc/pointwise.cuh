@@ -45,9 +45,14 @@ __global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadA
 
 // One correction term: cE*(A - Ap) + cI*(D - Dp)                 (R == nullptr)
 //                   or cE*(A - Ap) + cI*(D - Dp + R - Rp)
+// CISDCQ difference cache: a term whose differences dA = A - Ap and dDR = ((D - Dp) + R) - Rp were
+// stored by an earlier launch reads just those two fields (diff != 0: A = dA, D = dDR); a term
+// read in full can store them (outA/outDR) for the later nodes.  Same operations, same bits.
 struct RhsTerm {
   double cE, cI;
   const double *A, *Ap, *D, *Dp, *R, *Rp;
+  int diff;
+  double *outA, *outDR;
 };
 
 enum RhsKind {
@@ -108,7 +113,19 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
   for (int t = 0; t < kMaxM; ++t) {
     if (t >= a.nt) break;
     const RhsTerm& T = a.t[t];
-    r += T.cE * (T.A[e] - T.Ap[e]) + T.cI * (T.D[e] - T.Dp[e] + T.R[e] - T.Rp[e]);
+    double dA, dDR;
+    if (T.diff) {
+      dA = T.A[e];
+      dDR = T.D[e];
+    } else {
+      dA = T.A[e] - T.Ap[e];
+      dDR = T.D[e] - T.Dp[e] + T.R[e] - T.Rp[e];
+      if (T.outA) {
+        T.outA[e] = dA;
+        T.outDR[e] = dDR;
+      }
+    }
+    r += T.cE * dA + T.cI * dDR;
   }
   r += a.fc * (a.X[e] - a.Y[e]) - a.fc * a.Z[e];
   a.out[e] = r;

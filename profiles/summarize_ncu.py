@@ -110,7 +110,11 @@ def main():
             lines.append(f"| {name} | " + " | ".join(cells) + f" | {gbs:.0f} |")
             cls = CLASS.get(base_name(r["kernel"]))
             if cls and cls not in traffic:
-                traffic[cls] = rd + wr
+                traffic[cls] = {"kernel": name, "dram_bytes": rd + wr, "time_us": t,
+                                "dram_pct": r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                                "fp64_pipe_pct": r.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                                "l1_pct": r.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                                "source": f"profiles/{tag}/{tag}_{cfg}_{part}_raw.csv (first captured launch)"}
     lines.append("")
     with open(os.path.join(here, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
