@@ -8,6 +8,7 @@
 // swap after every sweep (the reference's fa_p = state.fa copy, integrators.cpp:74/108, becomes a
 // pointer swap), and node 0 is shared by both sets.  After SweepState::initialize every node of
 // the current set aliases node 0 (no M-fold copy).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -145,6 +146,11 @@ struct cisdc_gpu_ctx {
   unsigned long long newton_seen = 0, mg_seen = 0;
   cudaStream_t s_main = nullptr, s_r = nullptr;
   int num_sms = 148;
+  // optional SM partition for the PMISDC D/R chains (green contexts; CISDC_GREEN_R_SMS = SMs of the
+  // R chain): the two chains then run side by side instead of time-slicing the whole GPU
+  CUgreenCtx green[2] = {};
+  CUresult (*green_destroy)(CUgreenCtx) = nullptr;
+  cudaStream_t gs_d = nullptr, gs_r = nullptr;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t ev_base = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
   Timing tm;
@@ -770,6 +776,12 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   // cross-stream edges D(m,l) -> R(m,l) and R(m-2,l), R(m-1,l-1), R(m,l-1) -> D(m,l) are events.
   // D cells are totally ordered on their stream (single rhs buffer); R cells write only their slots.
   cudaStream_t sr = ctx->s_r;
+  if (ctx->gs_d) {  // partitioned SMs: both chains on their green streams, joined back into s_main
+    CU(cudaEventRecord(ctx->ev_base, sd));
+    CU(cudaStreamWaitEvent(ctx->gs_d, ctx->ev_base, 0));
+    sd = ctx->gs_d;
+    sr = ctx->gs_r;
+  }
   const size_t ncells = (size_t)M * nu;
   while (ctx->ev_pool.size() < 2 * ncells) {
     cudaEvent_t e;
@@ -796,6 +808,10 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   }
   CU(cudaEventRecord(ctx->ev_join, sr));
   CU(cudaStreamWaitEvent(sd, ctx->ev_join, 0));
+  if (sd != ctx->s_main) {
+    CU(cudaEventRecord(ctx->ev_join, sd));
+    CU(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
+  }
   return CISDC_OK;
 }
 
@@ -826,6 +842,49 @@ int fill_mass_action(const cisdc_problem_desc* d, Reaction& rx, std::string& why
     }
     rx.k[r] = d->rate_constants[r];
   }
+  return 0;
+}
+
+// Two green contexts over disjoint SM sets: `want` SMs (rounded by the driver) for the R chain, the
+// rest for the D chain; one stream in each.  Kernels of the runtime launch on these streams as on
+// any other (the green context is the primary context with a restricted SM set).
+int setup_green(cisdc_gpu_ctx* ctx, int want) {
+  // driver entry points through the runtime (no link-time dependency on libcuda)
+  auto sym = [](const char* name) -> void* {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return fn;
+  };
+  auto pDeviceGet = reinterpret_cast<CUresult (*)(CUdevice*, int)>(sym("cuDeviceGet"));
+  auto pGetRes = reinterpret_cast<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>(sym("cuDeviceGetDevResource"));
+  auto pSplit = reinterpret_cast<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*,
+                                              unsigned, unsigned)>(sym("cuDevSmResourceSplitByCount"));
+  auto pDesc = reinterpret_cast<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>(sym("cuDevResourceGenerateDesc"));
+  auto pCreate = reinterpret_cast<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>(sym("cuGreenCtxCreate"));
+  auto pStream = reinterpret_cast<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>(sym("cuGreenCtxStreamCreate"));
+  ctx->green_destroy = reinterpret_cast<CUresult (*)(CUgreenCtx)>(sym("cuGreenCtxDestroy"));
+  if (!pDeviceGet || !pGetRes || !pSplit || !pDesc || !pCreate || !pStream || !ctx->green_destroy) return 1;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  CUdevice cdev;
+  if (pDeviceGet(&cdev, dev) != CUDA_SUCCESS) return 1;
+  CUdevResource all{}, grp[1]{}, rest{};
+  if (pGetRes(cdev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return 1;
+  unsigned ng = 1;
+  if (pSplit(grp, &ng, &all, &rest, 0, (unsigned)want) != CUDA_SUCCESS || ng != 1) return 1;
+  CUdevResourceDesc dr, dd;
+  if (pDesc(&dr, &grp[0], 1) != CUDA_SUCCESS) return 1;
+  if (pDesc(&dd, &rest, 1) != CUDA_SUCCESS) return 1;
+  if (pCreate(&ctx->green[0], dd, cdev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return 1;
+  if (pCreate(&ctx->green[1], dr, cdev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return 1;
+  CUstream sd, sr;
+  if (pStream(&sd, ctx->green[0], CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return 1;
+  if (pStream(&sr, ctx->green[1], CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return 1;
+  ctx->gs_d = sd;
+  ctx->gs_r = sr;
+  std::fprintf(stderr, "cisdc: green contexts: D chain %u SMs, R chain %u SMs\n", rest.sm.smCount, grp[0].sm.smCount);
   return 0;
 }
 
@@ -895,6 +954,10 @@ void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
   if (ctx->s_r) cudaStreamDestroy(ctx->s_r);
+  if (ctx->gs_d) cudaStreamDestroy(ctx->gs_d);
+  if (ctx->gs_r) cudaStreamDestroy(ctx->gs_r);
+  for (CUgreenCtx g : ctx->green)
+    if (g && ctx->green_destroy) ctx->green_destroy(g);
   delete ctx;
 }
 
@@ -1064,6 +1127,10 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     const int mode = e ? std::atoi(e) : 1;
     CU(cudaStreamCreateWithPriority(&ctx->s_main, cudaStreamNonBlocking, mode == 1 ? hi : lo));
     CU(cudaStreamCreateWithPriority(&ctx->s_r, cudaStreamNonBlocking, mode == 2 ? hi : lo));
+    if (const char* g = std::getenv("CISDC_GREEN_R_SMS")) {
+      const int want = std::atoi(g);
+      if (want > 0 && setup_green(ctx, want) != 0) return set_err(ctx, CISDC_E_CUDA, "green context setup failed");
+    }
   }
   CU(cudaEventCreateWithFlags(&ctx->ev_base, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
