@@ -221,6 +221,15 @@ int eval_min_blocks() {
   return v;
 }
 
+// two cells per thread for F_A/F_D on even-nx 3-D grids (CISDC_EVAL_PAIR=0: one cell per thread)
+bool eval_pair() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_EVAL_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd, cudaStream_t s) {
   const Geom& g = ctx->g;
   const dim3 grid = stencil_grid(g.nx, g.ny, g.nz, g.S, g.ndim), block = stencil_block(g.ndim);
@@ -233,7 +242,20 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
         k_eval_ad<3><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd);
         break;
       }
-      if (ctx->ops.vconst)
+      if (g.nx % 2 == 0 && eval_pair()) {
+        static bool attr = false;
+        if (!attr) {
+          CU(cudaFuncSetAttribute(k_eval_ad3_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
+          CU(cudaFuncSetAttribute(k_eval_ad3_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
+          attr = true;
+        }
+        if (ctx->ops.vconst)
+          k_eval_ad3_pair<true><<<tile3d_pair_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), kPairSmem, s>>>(
+              ctx->ops, g, phi, fa, fd, kZChunk);
+        else
+          k_eval_ad3_pair<false><<<tile3d_pair_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), kPairSmem, s>>>(
+              ctx->ops, g, phi, fa, fd, kZChunk);
+      } else if (ctx->ops.vconst)
         k_eval_ad3_tiled<2, true><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa,
                                                                                                  fd, kZChunk);
       else if (eval_min_blocks() >= 3)

@@ -265,4 +265,230 @@ __global__ void __launch_bounds__(kTX* kTY, MINB) k_eval_ad3_tiled(Ops o, Geom g
       });
 }
 
+// ------------------------------------------------------------------------------------------------
+// Two x-adjacent cells per thread (F_A/F_D on grids with even nx): a (32, 8) block owns a 64 x 8
+// tile; the 68 x 12 halo tile of a plane is staged with 16-byte cp.async (pairs of cells never
+// straddle the periodic seam when nx is even), and each thread reads its x taps i-2 .. i+3 as three
+// 128-bit shared loads and its y taps / new z tap as 128-bit pairs: 8 shared loads per 2 cells
+// instead of 2 x 10 eight-byte ones.  The face between the two cells is shared (same bits: same
+// bracket operands, same face velocity).
+constexpr int kPTX = 2 * kTX;                 // 64 cells wide
+constexpr int kPTileW = kPTX + 2 * kHalo;     // 68
+constexpr int kPTileP = kPTileW;              // pitch (16-byte rows)
+constexpr int kPChunks = kPTileW / 2 * kTileH;  // 408 16-byte chunks per plane
+constexpr int kPChunkPer = (kPChunks + kTX * kTY - 1) / (kTX * kTY);  // 2
+constexpr int kPPlaneSlot = kTileH * kPTileP;   // 816 doubles
+constexpr size_t kPairSmem = (size_t)kRing * kPPlaneSlot * sizeof(double);  // 52 KB (dynamic)
+
+__device__ __forceinline__ void cp_async16(unsigned smem, const double* g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem), "l"(g) : "memory");
+}
+
+#ifndef __CUDACC_RTC__
+inline dim3 tile3d_pair_grid(int nx, int ny, int nz, int S) {
+  return dim3((unsigned)((nx + kPTX - 1) / kPTX), (unsigned)((ny + kTY - 1) / kTY),
+              (unsigned)(S * ((nz + kZChunk - 1) / kZChunk)));
+}
+#endif
+
+// Taps of a cell pair (i, i+1) at plane k: x[0..5] = i-2 .. i+3; y[c][o], z[c][o] = offsets o-2.
+struct PairTaps {
+  double x[6];
+  double y[2][5];
+  double z[2][5];
+};
+
+template <class PlaneFn, class Body>
+__device__ __forceinline__ void walk_pair(const double* __restrict__ f, int nx, int ny, int nz, const ZChunk& z,
+                                          double* ring, PlaneFn plane, Body body) {
+  const int i0 = blockIdx.x * kPTX, j0 = blockIdx.y * kTY;
+  const int i = i0 + 2 * threadIdx.x, j = j0 + threadIdx.y;
+  const int t = threadIdx.y * kTX + threadIdx.x;
+  const unsigned pl = (unsigned)nx * (unsigned)ny;
+  const bool in = i < nx && j < ny;  // nx even: i and i+1 are in or out together
+  const unsigned col = in ? (unsigned)j * (unsigned)nx + (unsigned)i : 0u;
+  f = opaque(f);
+  // staged chunks of this thread: smem slot (in doubles) and in-plane offset of the pair
+  int slot[kPChunkPer];
+  unsigned off[kPChunkPer];
+#pragma unroll
+  for (int u = 0; u < kPChunkPer; ++u) {
+    const int idx = t + u * kTX * kTY;
+    if (idx < kPChunks) {
+      const int r = idx / (kPTileW / 2), c2 = idx - r * (kPTileW / 2);
+      slot[u] = r * kPTileP + 2 * c2;
+      off[u] = (unsigned)wrap_any(j0 + r - kHalo, ny) * (unsigned)nx + (unsigned)wrap_any(i0 + 2 * c2 - kHalo, nx);
+    } else {
+      slot[u] = -1;
+      off[u] = 0;
+    }
+  }
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  auto issue = [&](int kk) {
+    if (kk <= z.k1 + 1) {
+      const double* fp = opaque(f + (unsigned)wrapi(kk, nz) * pl);
+      const unsigned sb = ring_s + (unsigned)((kk & (kRing - 1)) * kPPlaneSlot) * 8u;
+#pragma unroll
+      for (int u = 0; u < kPChunkPer; ++u)
+        if ((u + 1) * kTX * kTY <= kPChunks || slot[u] >= 0) cp_async16(sb + (unsigned)slot[u] * 8u, fp + off[u]);
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int kk = -2; kk <= 4; ++kk) issue(z.k0 + kk);
+  const int cidx = (threadIdx.y + kHalo) * kPTileP + 2 * threadIdx.x + kHalo;  // cell i in the tile
+  double q[2][5];
+  auto ld2 = [&](const double* p, double& a, double& b) {
+    const double2 v = *reinterpret_cast<const double2*>(p);
+    a = v.x;
+    b = v.y;
+  };
+  auto step = [&](auto ph, int k) {
+    constexpr int P = decltype(ph)::value;
+    cp_async_wait<2>();
+    __syncthreads();
+    issue(k + 5);
+    const double* tk = ring + (k & (kRing - 1)) * kPPlaneSlot;
+    ld2(ring + ((k + 2) & (kRing - 1)) * kPPlaneSlot + cidx, q[0][(P + 4) % 5], q[1][(P + 4) % 5]);
+    plane(k);
+    PairTaps v;
+    ld2(tk + cidx - 2, v.x[0], v.x[1]);
+    ld2(tk + cidx, v.x[2], v.x[3]);
+    ld2(tk + cidx + 2, v.x[4], v.x[5]);
+#pragma unroll
+    for (int o = 0; o < 5; ++o) {
+      if (o == 2) {
+        v.y[0][2] = v.x[2];
+        v.y[1][2] = v.x[3];
+      } else {
+        ld2(tk + cidx + (o - 2) * kPTileP, v.y[0][o], v.y[1][o]);
+      }
+      v.z[0][o] = q[0][(P + o) % 5];
+      v.z[1][o] = q[1][(P + o) % 5];
+    }
+    body(k, (unsigned)k * pl + col, v, in);
+  };
+  cp_async_wait<3>();
+  __syncthreads();
+#pragma unroll
+  for (int o = 0; o < 4; ++o) ld2(ring + ((z.k0 + o - 2) & (kRing - 1)) * kPPlaneSlot + cidx, q[0][o], q[1][o]);
+  for (int k = z.k0; k < z.k1; k += 5) {
+    step(Phase<0>{}, k);
+    if (k + 1 >= z.k1) break;
+    step(Phase<1>{}, k + 1);
+    if (k + 2 >= z.k1) break;
+    step(Phase<2>{}, k + 2);
+    if (k + 3 >= z.k1) break;
+    step(Phase<3>{}, k + 3);
+    if (k + 4 >= z.k1) break;
+    step(Phase<4>{}, k + 4);
+  }
+  cp_async_wait<0>();
+}
+
+// F_A and/or F_D, 3-D periodic, two cells per thread (nx even); UCONST as k_eval_ad3_tiled.
+template <bool UCONST>
+__global__ void __launch_bounds__(kTX* kTY, 2) k_eval_ad3_pair(Ops o, Geom g, const double* __restrict__ phi,
+                                                               double* __restrict__ fa, double* __restrict__ fd, int kc) {
+  extern __shared__ __align__(16) double pring[];
+  const ZChunk z = zchunk(g.nz, kc);
+  const long long sbase = (long long)z.s * g.ncell;
+  double* fas = fa ? opaque(fa + sbase) : nullptr;
+  double* fds = fd ? opaque(fd + sbase) : nullptr;
+  const int s = z.s;
+  const int ic = min(blockIdx.x * kPTX + 2 * threadIdx.x, g.nx - 2);
+  const int jc = min(blockIdx.y * kTY + threadIdx.y, g.ny - 1);
+  // face-velocity factors per cell c of the pair (face_u order: (T0 T1) T2); for a = 0 the left
+  // face of cell 1 is the right face of cell 0 (same product)
+  double pr[2][3], pl[2][3];
+  const double* t2[3];
+  bool adv[3];
+  double cd[3], ca[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    adv[a] = o.adv[a] != 0;
+    cd[a] = o.cdiff[s][a];
+    ca[a] = o.cadv[a];
+    t2[a] = o.vel[a][2];
+    if (UCONST) continue;
+    const double* t0 = o.vel[a][0];
+    const double* t1 = o.vel[a][1];
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int icc = ic + c;
+      const int il = a == 0 ? wrapi(icc - 1, g.nx) : icc, jl = a == 1 ? wrapi(jc - 1, g.ny) : jc;
+      pr[c][a] = (t0 ? __ldg(t0 + icc) : 1.0) * (t1 ? __ldg(t1 + jc) : 1.0);
+      pl[c][a] = (t0 ? __ldg(t0 + il) : 1.0) * (t1 ? __ldg(t1 + jl) : 1.0);
+    }
+  }
+  double t2r[3], t2l[3];
+  double fz_carry[2] = {0.0, 0.0};
+  int carry_k = -1;
+  walk_pair(
+      phi + sbase, g.nx, g.ny, g.nz, z, pring,
+      [&](int k) {
+        if (UCONST) return;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          t2r[a] = t2[a] ? __ldg(t2[a] + k) : 1.0;
+          t2l[a] = t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0;
+        }
+      },
+      [&](int k, unsigned cell, const PairTaps& v, bool ok) {
+        // per-cell 5-tap views: x taps of cell c are v.x[c .. c+4]
+        if (fas) {
+          double acc[2] = {0.0, 0.0};
+          // axis 0: faces i-1/2, i+1/2, i+3/2
+          if (adv[0]) {
+            const double u_l0 = UCONST ? o.ucon[0] : pl[0][0] * t2l[0];
+            const double u_m = UCONST ? o.ucon[0] : pr[0][0] * t2r[0];
+            const double u_r1 = UCONST ? o.ucon[0] : pr[1][0] * t2r[0];
+            const double f_l0 = u_l0 * (7.0 * (v.x[1] + v.x[2]) - (v.x[0] + v.x[3]));
+            const double f_m = u_m * (7.0 * (v.x[2] + v.x[3]) - (v.x[1] + v.x[4]));
+            const double f_r1 = u_r1 * (7.0 * (v.x[3] + v.x[4]) - (v.x[2] + v.x[5]));
+            acc[0] = acc[0] + (f_m - f_l0) * ca[0];
+            acc[1] = acc[1] + (f_r1 - f_m) * ca[0];
+          }
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            if (adv[1]) {
+              const double ur = UCONST ? o.ucon[1] : pr[c][1] * t2r[1];
+              const double ul = UCONST ? o.ucon[1] : pl[c][1] * t2l[1];
+              const double fr = ur * (7.0 * (v.y[c][2] + v.y[c][3]) - (v.y[c][1] + v.y[c][4]));
+              const double fl = ul * (7.0 * (v.y[c][1] + v.y[c][2]) - (v.y[c][0] + v.y[c][3]));
+              acc[c] = acc[c] + (fr - fl) * ca[1];
+            }
+            if (adv[2]) {
+              const double ur = UCONST ? o.ucon[2] : pr[c][2] * t2r[2];
+              const double fr = ur * (7.0 * (v.z[c][2] + v.z[c][3]) - (v.z[c][1] + v.z[c][4]));
+              double fl;
+              if (carry_k == k) {
+                fl = fz_carry[c];
+              } else {
+                const double ul = UCONST ? o.ucon[2] : pl[c][2] * t2l[2];
+                fl = ul * (7.0 * (v.z[c][1] + v.z[c][2]) - (v.z[c][0] + v.z[c][3]));
+              }
+              fz_carry[c] = fr;
+              acc[c] = acc[c] + (fr - fl) * ca[2];
+            }
+          }
+          if (ok) {
+            __stcg(reinterpret_cast<double2*>(fas + cell), make_double2(-acc[0], -acc[1]));
+          }
+        }
+        if (fds) {
+          double lap[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            lap[c] = 0.0;
+            lap[c] = lap[c] + cd[0] * lap5(v.x[c], v.x[c + 1], v.x[c + 2], v.x[c + 3], v.x[c + 4]);
+            lap[c] = lap[c] + cd[1] * lap5(v.y[c][0], v.y[c][1], v.y[c][2], v.y[c][3], v.y[c][4]);
+            lap[c] = lap[c] + cd[2] * lap5(v.z[c][0], v.z[c][1], v.z[c][2], v.z[c][3], v.z[c][4]);
+          }
+          if (ok) __stcg(reinterpret_cast<double2*>(fds + cell), make_double2(lap[0], lap[1]));
+        }
+        carry_k = k + 1;
+      });
+}
+
 }  // namespace cisdc_b200
