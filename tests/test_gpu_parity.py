@@ -289,11 +289,12 @@ def random_velocity_tables(n, seed=3):
 
 
 @pytest.mark.parametrize("n,variable", [((40, 20, 36), True), ((40, 20, 36), False), ((16, 8, 70), True),
-                                         ((64, 24, 33), False)])
+                                         ((64, 24, 33), False), ((37, 20, 36), True), ((37, 12, 40), False)])
 def test_tiled_3d_ragged_and_variable_velocity(gpu, oracle, n, variable):
     """The tiled 3-D F_A/F_D and multigrid kernels (cp.async plane ring, z carry, uniform-velocity
-    specialisation) on grids that are not multiples of the 32 x 8 tile or the 32-plane chunk, with
-    spatially varying (general path) or uniform (specialised path) face velocities: bitwise."""
+    specialisation; two cells per thread for even nx, one for odd nx) on grids that are not
+    multiples of the tiles or the 32-plane chunk, with spatially varying (general path) or uniform
+    (specialised path) face velocities: bitwise."""
     vel = random_velocity_tables(n) if variable else P.constant_velocity_tables((1.0, -0.5, 0.25), n)
     spec = c5_like(n, vel)
     for workers in (0, 2):
