@@ -300,3 +300,22 @@ def test_tiled_3d_ragged_and_variable_velocity(gpu, oracle, n, variable):
     for workers in (0, 2):
         _, g, c = per_step_compare(oracle, spec, 2, 1, workers=workers)
         assert np.array_equal(g, c)
+
+
+# ------------------------------------------------------------------ shared-reciprocal division (newton.cuh)
+
+def test_div_rcp_bitexact(gpu, tmp_path):
+    """div_rcp(a, b, rcp_refined(b)) == IEEE a / b bit for bit (5 x 2^26 operand pairs: ordinary,
+    extreme exponents, binade edges, near-midpoint quotients, zeros / infinities / NaN)."""
+    import os
+    import shutil
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    exe = str(tmp_path / "div_check")
+    subprocess.run([nvcc, "-std=c++17", "-O3", "-gencode", "arch=compute_100a,code=sm_100a", "-fmad=false",
+                    "-I", os.path.join(root, "include"), "-I", os.path.join(root, "paper_1801_01201_b200", "csrc"),
+                    os.path.join(root, "tests", "cuda", "div_check.cu"), "-o", exe], check=True, capture_output=True)
+    out = subprocess.run([exe, str(1 << 26)], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
