@@ -20,6 +20,11 @@
  *   cisdc_gpu_integrate           <- cisdc::integrate                  proj/core/src/integrators.cpp:301-333
  *   cisdc_gpu_eval / cisdc_gpu_solve
  *                                 <- OperatorSplitProblem::eval_* / solve_* (one stage on one field)
+ *   cisdc_gpu_last_trace          <- the ScheduleTrace returned by cisdc::execute_pipelined
+ *                                    proj/core/include/cisdc/pipeline.hpp:72-93
+ *   cisdc_write_field_snapshot / cisdc_read_field_snapshot
+ *                                 <- cisdc::write_field_snapshot / read_field_snapshot
+ *                                    proj/core/src/problems/reaction_diffusion.cpp:230-259
  *
  * Error behaviour mirrors the reference's exception taxonomy (proj/core/include/cisdc/errors.hpp:24-45):
  * every function returns a cisdc_status; the message (stage, node, first failing cell) is
@@ -45,7 +50,8 @@ typedef enum {
   CISDC_E_SOLVE = 3,            /* cisdc::SolveError */
   CISDC_E_NUMERIC = 4,          /* cisdc::NumericError (Newton / multigrid cap) */
   CISDC_E_CAPABILITY = 5,       /* cisdc::CapabilityError */
-  CISDC_E_CUDA = 6              /* CUDA runtime failure, out of memory */
+  CISDC_E_CUDA = 6,             /* CUDA runtime failure, out of memory */
+  CISDC_E_IO = 7                /* std::runtime_error of the snapshot / trace file IO */
 } cisdc_status;
 
 /* cisdc::Scheme, same order (proj/core/include/cisdc/integrators.hpp:30) */
@@ -202,6 +208,34 @@ double cisdc_gpu_device_time_ms(cisdc_gpu_ctx* ctx, int reset);
 long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx);
 /* FP64 pipe peak on the current device: DFMA chains and DMUL+DADD chains, TFLOP/s */
 int cisdc_gpu_fp64_peak(double* tflops_dfma, double* tflops_dmul_dadd);
+/* ---- PMISDC schedule trace (cisdc::CellTrace / ScheduleTrace, pipeline.hpp:72-84) ----
+   With tracing on, every CISDCQ sweep run with workers > 0 records GPU timestamps at the start and
+   end of each DAG cell on its stream (worker 0 = diffusion stream, 1 = reaction stream).
+   cisdc_gpu_last_trace returns the cells of the last such sweep in cell-id order
+   (TaskGraph::cell_id); times are ns from the sweep's first cell, seq_* a single global order of
+   the start/end events (ends before starts on equal times). */
+typedef struct {
+  int kind; /* 0 = diffusion (D), 1 = reaction (R) */
+  int m;
+  int ell;
+  int worker;
+  long long start_ns, end_ns;
+  long long seq_start, seq_end;
+} cisdc_cell_trace;
+int cisdc_gpu_set_trace(cisdc_gpu_ctx* ctx, int on);
+/* copies min(n, max_cells) cells; *n_cells = n, *workers = streams used (0 if no traced sweep) */
+int cisdc_gpu_last_trace(cisdc_gpu_ctx* ctx, cisdc_cell_trace* cells, int max_cells, int* n_cells, int* workers);
+
+/* ---- field snapshots (host only; reaction_diffusion.hpp:101-112) ----
+   File: magic "SDC1", u32 n_x, f64 dx, then n_x doubles, little-endian.  write: n must equal n_x
+   (CISDC_E_INVALID_ARGUMENT, "size mismatch"), IO failure -> CISDC_E_IO.  read: header into
+   *n_x, *dx, then min(n_x, cap) values into data (data may be NULL to query the size); bad magic or
+   a truncated file -> CISDC_E_IO.  cisdc_io_last_error(): the message of the calling thread's last
+   failed snapshot call, worded as the reference's exceptions. */
+int cisdc_write_field_snapshot(const char* path, int n_x, double dx, const double* data, size_t n);
+int cisdc_read_field_snapshot(const char* path, int* n_x, double* dx, double* data, size_t cap);
+const char* cisdc_io_last_error(void);
+
 /* Generate and NVRTC-compile the network-specialised Newton kernels of a mass-action problem for
    sm_100a without loading them (no GPU needed); the compiler log goes to log[cap]. */
 int cisdc_rtc_compile_check(const cisdc_problem_desc* desc, char* log, size_t cap);

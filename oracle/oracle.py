@@ -93,6 +93,11 @@ def ref_lib() -> C.CDLL | None:
                                    C.c_int, C.c_int, _dp, _dp, _dp, C.POINTER(_abi.CountersC), _cp]
         lib.ref_stage.argtypes = [C.POINTER(_abi.ProblemDescC), C.c_int, C.c_int, C.c_double, _dp, _dp, _cp]
         lib.ref_rd_initial_condition.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, _dp]
+        lib.ref_write_field_snapshot.argtypes = [C.c_char_p, C.c_int, C.c_double, _dp, C.c_size_t, _cp]
+        lib.ref_read_field_snapshot.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), _dp,
+                                                C.c_size_t, _cp]
+        tp = C.POINTER(_abi.CellTraceC)
+        lib.ref_validate_trace.argtypes = [C.c_int, C.c_int, C.c_int, tp, C.c_int, _cp, C.c_size_t]
         _ref = lib
     return _ref
 
@@ -269,3 +274,41 @@ def ref_stage(desc, solve: bool, stage: int, coef: float, x: np.ndarray) -> np.n
     if rc:
         raise OracleError(rc, err.value.decode())
     return out
+
+
+# ---------------------------------------------------------------- snapshot IO / schedule traces (reference)
+
+def ref_write_field_snapshot(path: str, n_x: int, dx: float, data) -> None:
+    a = np.ascontiguousarray(data, dtype=np.float64)
+    err = C.create_string_buffer(1024)
+    rc = ref_lib().ref_write_field_snapshot(str(path).encode(), int(n_x), float(dx), _dp_of(a), a.size, err)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+
+
+def ref_read_field_snapshot(path: str):
+    n, dx = C.c_int(), C.c_double()
+    err = C.create_string_buffer(1024)
+    rc = ref_lib().ref_read_field_snapshot(str(path).encode(), C.byref(n), C.byref(dx), None, 0, err)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    out = np.empty(n.value)
+    ref_lib().ref_read_field_snapshot(str(path).encode(), C.byref(n), C.byref(dx), _dp_of(out), out.size, err)
+    return n.value, dx.value, out
+
+
+def _trace_arrays(trace):
+    buf = (_abi.CellTraceC * max(len(trace.cells), 1))()
+    for i, c in enumerate(trace.cells):
+        buf[i].kind, buf[i].m, buf[i].ell, buf[i].worker = int(c.cell.kind), c.cell.m, c.cell.ell, c.worker
+        buf[i].start_ns, buf[i].end_ns, buf[i].seq_start, buf[i].seq_end = c.start_ns, c.end_ns, c.seq_start, c.seq_end
+    return buf
+
+
+def ref_validate_schedule_trace(M: int, nu: int, trace) -> str:
+    """The reference's validate_schedule_trace (pipeline.cpp:322-350) on a trace in cell-id order."""
+    msg = C.create_string_buffer(1024)
+    rc = ref_lib().ref_validate_trace(M, nu, trace.workers, _trace_arrays(trace), len(trace.cells), msg, 1024)
+    if rc:
+        raise OracleError(rc, msg.value.decode())
+    return msg.value.decode()

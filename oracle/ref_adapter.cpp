@@ -10,6 +10,7 @@
 // wrapped here as a cisdc::OperatorSplitProblem subclass (AdrProblem) whose stages call the
 // oracle's problem class, so the reference's own integrators (cisdc::integrate, run_sweep,
 // execute_pipelined) drive it unmodified.
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstring>
@@ -319,6 +320,64 @@ int ref_rd_initial_condition(int n_x, double a, double d, double r, double* out)
     std::memcpy(out, v.data(), sizeof(double) * n_x);
     return CISDC_OK;
   } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// SDC1 snapshot IO of the reference (reaction_diffusion.cpp:230-259), for byte-level checks.
+int ref_write_field_snapshot(const char* path, int n_x, double dx, const double* data, size_t n, char* err) {
+  try {
+    cisdc::write_field_snapshot(path, n_x, dx, std::span<const double>(data, n));
+    return CISDC_OK;
+  } catch (const std::invalid_argument& e) {
+    if (err) std::snprintf(err, 1024, "%s", e.what());
+    return CISDC_E_INVALID_ARGUMENT;
+  } catch (const std::exception& e) {
+    if (err) std::snprintf(err, 1024, "%s", e.what());
+    return CISDC_E_IO;
+  }
+}
+
+int ref_read_field_snapshot(const char* path, int* n_x, double* dx, double* data, size_t cap, char* err) {
+  try {
+    const cisdc::FieldSnapshot s = cisdc::read_field_snapshot(path);
+    *n_x = s.n_x;
+    *dx = s.dx;
+    if (data) std::memcpy(data, s.data.data(), sizeof(double) * std::min<size_t>(cap, s.data.size()));
+    return CISDC_OK;
+  } catch (const std::exception& e) {
+    if (err) std::snprintf(err, 1024, "%s", e.what());
+    return CISDC_E_IO;
+  }
+}
+
+// The reference's validate_schedule_trace (pipeline.cpp:322-350) on a trace given as arrays in
+// cell-id order; msg receives its verdict ("" = valid).
+static cisdc::ScheduleTrace to_ref_trace(int M, int nu, int workers, const cisdc_cell_trace* cells, int n) {
+  const cisdc::TaskGraph g = cisdc::build_task_graph(M, nu);
+  cisdc::ScheduleTrace t;
+  t.workers = workers;
+  for (int i = 0; i < n; ++i) {
+    cisdc::CellTrace c;
+    c.cell = g.cells[i];
+    c.worker = cells[i].worker;
+    c.start_ns = cells[i].start_ns;
+    c.end_ns = cells[i].end_ns;
+    c.seq_start = cells[i].seq_start;
+    c.seq_end = cells[i].seq_end;
+    t.cells.push_back(c);
+  }
+  return t;
+}
+
+int ref_validate_trace(int M, int nu, int workers, const cisdc_cell_trace* cells, int n, char* msg, size_t cap) {
+  try {
+    const cisdc::TaskGraph g = cisdc::build_task_graph(M, nu);
+    const std::string v = cisdc::validate_schedule_trace(g, to_ref_trace(M, nu, workers, cells, n));
+    std::snprintf(msg, cap, "%s", v.c_str());
+    return CISDC_OK;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, cap, "%s", e.what());
     return code_of(e);
   }
 }

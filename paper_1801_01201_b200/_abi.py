@@ -8,7 +8,7 @@ MAX_M = 8
 MAX_SPECIES = 16
 MAX_REACTIONS = 64
 
-OK, E_INVALID_ARGUMENT, E_FACTORIZATION, E_SOLVE, E_NUMERIC, E_CAPABILITY, E_CUDA = range(7)
+OK, E_INVALID_ARGUMENT, E_FACTORIZATION, E_SOLVE, E_NUMERIC, E_CAPABILITY, E_CUDA, E_IO = range(8)
 PROBLEM_PERIODIC_ADR, PROBLEM_REFERENCE_RD, PROBLEM_LINEAR_SCALAR = 0, 1, 2
 REACTION_NONE, REACTION_LINEAR_DECAY, REACTION_BISTABLE, REACTION_MASS_ACTION = 0, 1, 2, 3
 DIFFUSION_DIRECT, DIFFUSION_MULTIGRID, DIFFUSION_BANDED_ORACLE = 0, 1, 2
@@ -97,6 +97,12 @@ class StepReportC(C.Structure):
 
 # C-ABI symbols of include/cisdc_gpu.h: (name, restype, argtypes)
 _vp = C.c_void_p
+class CellTraceC(C.Structure):
+    _fields_ = [("kind", C.c_int), ("m", C.c_int), ("ell", C.c_int), ("worker", C.c_int),
+                ("start_ns", C.c_longlong), ("end_ns", C.c_longlong),
+                ("seq_start", C.c_longlong), ("seq_end", C.c_longlong)]
+
+
 GPU_SYMBOLS = [
     ("cisdc_make_quadrature_tables", C.c_int, [C.c_int, C.c_int, C.POINTER(TablesC)]),
     ("cisdc_gpu_create", C.c_int, [C.POINTER(ProblemDescC), C.POINTER(TablesC), C.POINTER(_vp)]),
@@ -123,6 +129,11 @@ GPU_SYMBOLS = [
     ("cisdc_gpu_launch_count", C.c_longlong, [_vp]),
     ("cisdc_gpu_fp64_peak", C.c_int, [_dp, _dp]),
     ("cisdc_rtc_compile_check", C.c_int, [C.POINTER(ProblemDescC), C.c_char_p, C.c_size_t]),
+    ("cisdc_gpu_set_trace", C.c_int, [_vp, C.c_int]),
+    ("cisdc_gpu_last_trace", C.c_int, [_vp, C.POINTER(CellTraceC), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    ("cisdc_write_field_snapshot", C.c_int, [C.c_char_p, C.c_int, C.c_double, _dp, C.c_size_t]),
+    ("cisdc_read_field_snapshot", C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), _dp, C.c_size_t]),
+    ("cisdc_io_last_error", C.c_char_p, []),
 ]
 
 _LIB = None

@@ -9,6 +9,10 @@ Same names, argument meaning and error behaviour as proj/core/include/cisdc/*.hp
   GpuProblem (OperatorSplitProblem stages)    operator_split.hpp:36-54
   SweepState (device resident)                sweep_state.hpp:33-53
   run_sweep / execute_pipelined / integrate   integrators.cpp:290-333, pipeline.cpp:171-320
+  Cell / TaskGraph / build_task_graph         pipeline.hpp:26-50, pipeline.cpp:36-70
+  CellTrace / ScheduleTrace                   pipeline.hpp:72-84 (GPU: per-cell stream timestamps)
+  validate_schedule_trace / write_trace_csv   pipeline.cpp:322-361
+  write_field_snapshot / read_field_snapshot  reaction_diffusion.cpp:230-259 ("SDC1" files)
   FactorizationError / SolveError / NumericError / CapabilityError   errors.hpp:24-45
 
 Every call goes through the C-ABI of include/cisdc_gpu.h into libcisdc_gpu.so; nothing here
@@ -59,6 +63,7 @@ class CudaError(RuntimeError):
 
 
 _ERRORS = {
+    _abi.E_IO: RuntimeError,
     _abi.E_INVALID_ARGUMENT: ValueError,
     _abi.E_FACTORIZATION: FactorizationError,
     _abi.E_SOLVE: SolveError,
@@ -309,11 +314,171 @@ def run_sweep(scheme: int, state: SweepState, dt: float, nu: int = 1, counters: 
         counters.add_c(c)
 
 
+class CellKind(enum.IntEnum):
+    diffusion = 0
+    reaction = 1
+
+
+@dataclass(frozen=True)
+class Cell:
+    kind: CellKind
+    m: int
+    ell: int
+
+
+def cell_label(c: Cell) -> str:
+    """pipeline.cpp cell_label: D(m,ell) / R(m,ell)."""
+    return f"{'D' if c.kind == CellKind.diffusion else 'R'}({c.m},{c.ell})"
+
+
+@dataclass
+class TaskGraph:
+    M: int
+    nu: int
+    cells: list
+    dependencies: list
+    dependents: list
+
+    def cell_id(self, kind: int, m: int, ell: int) -> int:
+        return 2 * ((ell - 1) * self.M + (m - 1)) + (1 if kind == CellKind.reaction else 0)
+
+
+def build_task_graph(M: int, nu: int) -> TaskGraph:
+    """The CISDCQ-nu cell DAG (pipeline.cpp:36-70):
+    D(m,l) <- D(m-1,l), R(m-2,l), R(m-1,l-1), R(m,l-1);  R(m,l) <- D(m,l), R(m-1,l)."""
+    if M < 1 or nu < 1:
+        raise ValueError("build_task_graph: M and nu must be >= 1")
+    g = TaskGraph(M, nu, [], [], [])
+    for ell in range(1, nu + 1):
+        for m in range(1, M + 1):
+            g.cells += [Cell(CellKind.diffusion, m, ell), Cell(CellKind.reaction, m, ell)]
+    g.dependencies = [[] for _ in g.cells]
+    g.dependents = [[] for _ in g.cells]
+
+    def edge(u, v):
+        g.dependencies[v].append(u)
+        g.dependents[u].append(v)
+
+    for ell in range(1, nu + 1):
+        for m in range(1, M + 1):
+            d, r = g.cell_id(CellKind.diffusion, m, ell), g.cell_id(CellKind.reaction, m, ell)
+            if m >= 2:
+                edge(g.cell_id(CellKind.diffusion, m - 1, ell), d)
+            if m >= 3:
+                edge(g.cell_id(CellKind.reaction, m - 2, ell), d)
+            if ell >= 2:
+                if m >= 2:
+                    edge(g.cell_id(CellKind.reaction, m - 1, ell - 1), d)
+                edge(g.cell_id(CellKind.reaction, m, ell - 1), d)
+            edge(d, r)
+            if m >= 2:
+                edge(g.cell_id(CellKind.reaction, m - 1, ell), r)
+    return g
+
+
+@dataclass
+class CellTrace:
+    cell: Cell
+    worker: int
+    start_ns: int
+    end_ns: int
+    seq_start: int
+    seq_end: int
+
+
+@dataclass
+class ScheduleTrace:
+    """pipeline.hpp:81-84.  On the GPU a worker is a stream (0: diffusion, 1: reaction) and the
+    times are GPU event timestamps from the sweep's first cell."""
+    workers: int
+    cells: list
+
+
+def validate_schedule_trace(graph: TaskGraph, trace: ScheduleTrace) -> str:
+    """pipeline.cpp:322-350: '' if every DAG edge is respected in time and in the global order and
+    no worker runs two cells at once, else the first violation."""
+    n = len(graph.cells)
+    if len(trace.cells) != n:
+        return "trace size does not match graph"
+    for v in range(n):
+        for u in graph.dependencies[v]:
+            if trace.cells[u].end_ns > trace.cells[v].start_ns or trace.cells[u].seq_end > trace.cells[v].seq_start:
+                return f"edge violated: {cell_label(graph.cells[u])} -> {cell_label(graph.cells[v])}"
+    by_worker = [[] for _ in range(trace.workers)]
+    for c in trace.cells:
+        if c.worker < 0 or c.worker >= trace.workers:
+            return "bad worker id in trace"
+        by_worker[c.worker].append(c)
+    for w in by_worker:
+        w.sort(key=lambda c: c.start_ns)
+        for a, b in zip(w, w[1:]):
+            if b.start_ns < a.end_ns:
+                return f"worker overlap: {cell_label(a.cell)} and {cell_label(b.cell)}"
+    return ""
+
+
+def write_trace_csv(path: str, trace: ScheduleTrace) -> None:
+    """pipeline.cpp:352-361 schema: cell,kind,m,ell,worker,start_ns,end_ns."""
+    try:
+        f = open(path, "w")
+    except OSError:
+        raise RuntimeError("write_trace_csv: cannot open " + path) from None
+    with f:
+        f.write("cell,kind,m,ell,worker,start_ns,end_ns\n")
+        for c in trace.cells:
+            f.write(f"{cell_label(c.cell)},{'D' if c.cell.kind == CellKind.diffusion else 'R'},{c.cell.m},"
+                    f"{c.cell.ell},{c.worker},{c.start_ns},{c.end_ns}\n")
+
+
+def last_schedule_trace(ctx: "GpuContext") -> ScheduleTrace:
+    n, w = C.c_int(), C.c_int()
+    ctx.check(ctx.lib.cisdc_gpu_last_trace(ctx.h, None, 0, C.byref(n), C.byref(w)))
+    buf = (_abi.CellTraceC * max(n.value, 1))()
+    ctx.check(ctx.lib.cisdc_gpu_last_trace(ctx.h, buf, n.value, C.byref(n), C.byref(w)))
+    cells = [CellTrace(Cell(CellKind(c.kind), c.m, c.ell), c.worker, c.start_ns, c.end_ns, c.seq_start, c.seq_end)
+             for c in buf[: n.value]]
+    return ScheduleTrace(w.value, cells)
+
+
 def execute_pipelined(state: SweepState, dt: float, nu: int, workers: int = 2,
-                      counters: Optional[SolveCounters] = None) -> None:
+                      counters: Optional[SolveCounters] = None) -> ScheduleTrace:
+    """pipeline.cpp:171-320: one CISDCQ-nu sweep as the cell DAG (here: two CUDA streams with event
+    edges), bitwise equal to cisdcq_sweep; returns the schedule trace of the run."""
     if workers < 1:
         raise ValueError("execute_pipelined: workers must be >= 1")
-    run_sweep(Scheme.cisdcq, state, dt, nu, counters, workers)
+    state.ctx.check(state.ctx.lib.cisdc_gpu_set_trace(state.ctx.h, 1))
+    try:
+        run_sweep(Scheme.cisdcq, state, dt, nu, counters, workers)
+        return last_schedule_trace(state.ctx)
+    finally:
+        state.ctx.lib.cisdc_gpu_set_trace(state.ctx.h, 0)
+
+
+@dataclass
+class FieldSnapshot:
+    n_x: int
+    dx: float
+    data: np.ndarray
+
+
+def write_field_snapshot(path: str, n_x: int, dx: float, data) -> None:
+    """reaction_diffusion.cpp:230-244 ("SDC1", u32 n_x, f64 dx, n_x doubles)."""
+    lib = _abi.load()
+    a = np.ascontiguousarray(data, dtype=np.float64)
+    rc = lib.cisdc_write_field_snapshot(str(path).encode(), int(n_x), float(dx), _abi.dptr(a), a.size)
+    raise_for(rc, lib.cisdc_io_last_error().decode())
+
+
+def read_field_snapshot(path: str) -> FieldSnapshot:
+    """reaction_diffusion.cpp:246-259."""
+    lib = _abi.load()
+    n, dx = C.c_int(), C.c_double()
+    rc = lib.cisdc_read_field_snapshot(str(path).encode(), C.byref(n), C.byref(dx), None, 0)
+    raise_for(rc, lib.cisdc_io_last_error().decode())
+    out = np.empty(n.value)
+    rc = lib.cisdc_read_field_snapshot(str(path).encode(), C.byref(n), C.byref(dx), _abi.dptr(out), out.size)
+    raise_for(rc, lib.cisdc_io_last_error().decode())
+    return FieldSnapshot(n.value, dx.value, out)
 
 
 def integrate(problem_desc, phi0: np.ndarray, opt: IntegrateOptions, ctx: Optional[GpuContext] = None) -> IntegrateResult:

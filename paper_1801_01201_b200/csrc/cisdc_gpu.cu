@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -148,6 +149,11 @@ struct cisdc_gpu_ctx {
   int num_sms = 148;
   // optional SM partition for the PMISDC D/R chains (green contexts; CISDC_GREEN_R_SMS = SMs of the
   // R chain): the two chains then run side by side instead of time-slicing the whole GPU
+  // PMISDC schedule trace (cisdc_gpu_set_trace / cisdc_gpu_last_trace)
+  bool trace_on = false, trace_pending = false;
+  int trace_M = 0, trace_nu = 0, trace_workers = 0;
+  std::vector<cudaEvent_t> trace_ev;  // [2 * cell id + 0/1] start/end, last = base
+  std::vector<cisdc_cell_trace> trace;
   CUgreenCtx green[2] = {};
   CUresult (*green_destroy)(CUgreenCtx) = nullptr;
   cudaStream_t gs_d = nullptr, gs_r = nullptr;
@@ -812,6 +818,22 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   }
   auto evD = [&](int m, int ell) { return ctx->ev_pool[2 * ((size_t)(ell - 1) * M + (m - 1))]; };
   auto evR = [&](int m, int ell) { return ctx->ev_pool[2 * ((size_t)(ell - 1) * M + (m - 1)) + 1]; };
+  // trace: start/end events of cell id (TaskGraph::cell_id = 2 ((ell-1) M + (m-1)) + kind)
+  const bool tr = ctx->trace_on;
+  if (tr) {
+    while (ctx->trace_ev.size() < 4 * ncells + 1) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      ctx->trace_ev.push_back(e);
+    }
+    ctx->trace_M = M;
+    ctx->trace_nu = nu;
+    ctx->trace_workers = 2;
+    ctx->trace_pending = true;
+  }
+  auto tev = [&](int kind, int m, int ell, int end) {
+    return ctx->trace_ev[2 * (2 * ((size_t)(ell - 1) * M + (m - 1)) + kind) + end];
+  };
   CU(cudaEventRecord(ctx->ev_base, sd));
   CU(cudaStreamWaitEvent(sr, ctx->ev_base, 0));
   for (int ell = 1; ell <= nu; ++ell) {
@@ -821,10 +843,14 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
         if (m >= 2) CU(cudaStreamWaitEvent(sd, evR(m - 1, ell - 1), 0));
         CU(cudaStreamWaitEvent(sd, evR(m, ell - 1), 0));
       }
+      if (tr) CU(cudaEventRecord(tev(0, m, ell, 0), sd));
       TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c));
+      if (tr) CU(cudaEventRecord(tev(0, m, ell, 1), sd));
       CU(cudaEventRecord(evD(m, ell), sd));
       CU(cudaStreamWaitEvent(sr, evD(m, ell), 0));
+      if (tr) CU(cudaEventRecord(tev(1, m, ell, 0), sr));
       TRY(reaction_cell(ctx, W, m, ell, dt, sr, c));
+      if (tr) CU(cudaEventRecord(tev(1, m, ell, 1), sr));
       CU(cudaEventRecord(evR(m, ell), sr));
     }
   }
@@ -972,6 +998,7 @@ void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
   if (ctx->h_incr) cudaFreeHost(ctx->h_incr);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : ctx->trace_ev) cudaEventDestroy(e);
   for (cudaEvent_t e : {ctx->ev_base, ctx->ev_join, ctx->ev_t0, ctx->ev_t1})
     if (e) cudaEventDestroy(e);
   if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
@@ -1456,6 +1483,121 @@ int cisdc_gpu_fp64_peak(double* tflops_dfma, double* tflops_dmul_dadd) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(out);
+  return CISDC_OK;
+}
+
+int cisdc_gpu_set_trace(cisdc_gpu_ctx* ctx, int on) {
+  if (!ctx) return CISDC_E_INVALID_ARGUMENT;
+  ctx->trace_on = on != 0;
+  return CISDC_OK;
+}
+
+int cisdc_gpu_last_trace(cisdc_gpu_ctx* ctx, cisdc_cell_trace* cells, int max_cells, int* n_cells, int* workers) {
+  if (!ctx) return CISDC_E_INVALID_ARGUMENT;
+  if (ctx->trace_pending) {
+    const int M = ctx->trace_M, nu = ctx->trace_nu, n = 2 * M * nu;
+    CU(cudaStreamSynchronize(ctx->s_main));
+    CU(cudaStreamSynchronize(ctx->s_r));
+    if (ctx->gs_d) {
+      CU(cudaStreamSynchronize(ctx->gs_d));
+      CU(cudaStreamSynchronize(ctx->gs_r));
+    }
+    std::vector<double> t(2 * (size_t)n);
+    const cudaEvent_t base = ctx->trace_ev[0];  // start of D(1,1): the sweep's first cell
+    for (int id = 0; id < n; ++id)
+      for (int e = 0; e < 2; ++e) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, base, ctx->trace_ev[2 * id + e]));
+        t[2 * id + e] = (double)ms;
+      }
+    // one global order of all start/end events: by time, ends before starts on ties, then by id
+    std::vector<int> ord(2 * (size_t)n);
+    for (int i = 0; i < 2 * n; ++i) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](int a, int b) {
+      if (t[a] != t[b]) return t[a] < t[b];
+      if ((a & 1) != (b & 1)) return (a & 1) > (b & 1);
+      return a < b;
+    });
+    ctx->trace.assign(n, cisdc_cell_trace{});
+    for (int id = 0; id < n; ++id) {
+      cisdc_cell_trace& c = ctx->trace[id];
+      c.kind = id & 1;
+      c.m = (id >> 1) % M + 1;
+      c.ell = (id >> 1) / M + 1;
+      c.worker = c.kind;
+      c.start_ns = (long long)std::llround(t[2 * id] * 1e6);
+      c.end_ns = (long long)std::llround(t[2 * id + 1] * 1e6);
+    }
+    for (int r = 0; r < 2 * n; ++r) {
+      cisdc_cell_trace& c = ctx->trace[ord[r] >> 1];
+      if (ord[r] & 1) c.seq_end = r;
+      else c.seq_start = r;
+    }
+    ctx->trace_pending = false;
+  }
+  const int n = (int)ctx->trace.size();
+  if (n_cells) *n_cells = n;
+  if (workers) *workers = n ? ctx->trace_workers : 0;
+  if (cells)
+    for (int i = 0; i < n && i < max_cells; ++i) cells[i] = ctx->trace[i];
+  return CISDC_OK;
+}
+
+// ---- SDC1 field snapshots (reaction_diffusion.cpp:230-259), host only
+static thread_local std::string g_io_err;
+
+const char* cisdc_io_last_error(void) { return g_io_err.c_str(); }
+
+int cisdc_write_field_snapshot(const char* path, int n_x, double dx, const double* data, size_t n) {
+  if (!path || n_x < 0 || (size_t)n_x != n || (n && !data)) {
+    g_io_err = "write_field_snapshot: size mismatch";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    g_io_err = std::string("write_field_snapshot: cannot open ") + path;
+    return CISDC_E_IO;
+  }
+  const char magic[4] = {'S', 'D', 'C', '1'};
+  const uint32_t nn = (uint32_t)n_x;
+  bool ok = std::fwrite(magic, 1, 4, f) == 4 && std::fwrite(&nn, sizeof(nn), 1, f) == 1 &&
+            std::fwrite(&dx, sizeof(dx), 1, f) == 1 && (n == 0 || std::fwrite(data, sizeof(double), n, f) == n);
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) {
+    g_io_err = std::string("write_field_snapshot: write failed for ") + path;
+    return CISDC_E_IO;
+  }
+  return CISDC_OK;
+}
+
+int cisdc_read_field_snapshot(const char* path, int* n_x, double* dx, double* data, size_t cap) {
+  FILE* f = path ? std::fopen(path, "rb") : nullptr;
+  if (!f) {
+    g_io_err = std::string("read_field_snapshot: cannot open ") + (path ? path : "");
+    return CISDC_E_IO;
+  }
+  char magic[4];
+  if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "SDC1", 4) != 0) {
+    std::fclose(f);
+    g_io_err = std::string("read_field_snapshot: bad magic in ") + path;
+    return CISDC_E_IO;
+  }
+  uint32_t nn = 0;
+  double h = 0.0;
+  bool ok = std::fread(&nn, sizeof(nn), 1, f) == 1 && std::fread(&h, sizeof(h), 1, f) == 1;
+  std::vector<double> v;
+  if (ok) {
+    v.resize(nn);
+    ok = nn == 0 || std::fread(v.data(), sizeof(double), nn, f) == nn;
+  }
+  std::fclose(f);
+  if (!ok) {
+    g_io_err = std::string("read_field_snapshot: truncated file ") + path;
+    return CISDC_E_IO;
+  }
+  if (n_x) *n_x = (int)nn;
+  if (dx) *dx = h;
+  if (data) std::memcpy(data, v.data(), sizeof(double) * std::min<size_t>(cap, nn));
   return CISDC_OK;
 }
 

@@ -319,3 +319,28 @@ def test_div_rcp_bitexact(gpu, tmp_path):
     out = subprocess.run([exe, str(1 << 26)], capture_output=True, text=True, timeout=300)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+# ------------------------------------------------------------------ PMISDC schedule trace
+
+@pytest.mark.parametrize("nu", [1, 3])
+def test_gpu_schedule_trace_valid(gpu, oracle, nu):
+    """execute_pipelined on the GPU returns a ScheduleTrace (per-cell stream timestamps) that both the
+    Python validator and the reference's validate_schedule_trace accept, and the state equals the
+    serial cell order bitwise."""
+    spec = P.config_c5(scale=16)
+    st = api.SweepState(spec.problem, spec.M)
+    try:
+        st.initialize(spec.phi0)
+        tr = api.execute_pipelined(st, spec.dt, nu, workers=2)
+        piped = st.phi(spec.M)
+        g = api.build_task_graph(spec.M, nu)
+        assert len(tr.cells) == 2 * spec.M * nu and tr.workers == 2
+        assert api.validate_schedule_trace(g, tr) == ""
+        if oracle.ref_lib() is not None:
+            assert oracle.ref_validate_schedule_trace(spec.M, nu, tr) == ""
+        st.initialize(spec.phi0)
+        api.run_sweep(api.Scheme.cisdcq, st, spec.dt, nu)
+        assert np.array_equal(st.phi(spec.M), piped)
+    finally:
+        st.ctx.close()
