@@ -74,6 +74,7 @@ struct Timing final : LaunchHook {
     cur = take();
     cudaEventRecord(cur, s);
   }
+  void add_bytes(int cls, double b) override { bytes[cls] += b; }
   void after(int cls, cudaStream_t s, double b) override {
     ++launches;
     ++count[cls];

@@ -73,6 +73,8 @@ enum KernelClass {
 struct LaunchHook {
   virtual void before(int cls, cudaStream_t s) = 0;
   virtual void after(int cls, cudaStream_t s, double bytes) = 0;
+  // bytes known only after the fact (multigrid: per-species masking decided on the device)
+  virtual void add_bytes(int, double) {}
   virtual ~LaunchHook() = default;
 };
 #endif

@@ -461,6 +461,18 @@ struct MgRunner {
   bool check_next = false;          // the next level-0 sweep also reduces the residual norm of its input
   bool first_check = true;          // ... and ||b||_inf (the first check of the solve)
   DevStatus* st = nullptr;
+  // Compulsory bytes of one cycle for ALL species, per kernel class: the checking sweep (run for
+  // every species still active before the check) and the rest of the cycle (run for the species
+  // that continue).  Launches are charged 0 bytes; the solve charges sum_s of its per-species
+  // cycle counts afterwards (masked species move no data).
+  bool recording = false;
+  double fs_bytes = 0.0;
+  double rest_bytes[kNumKernelClasses] = {};
+  void charge(int cls, double b, bool is_check) {
+    if (!recording) return;
+    if (is_check) fs_bytes += b;
+    else rest_bytes[cls] += b;
+  }
 
   const double* bof(int l) const { return l == 0 ? b0 : h.lv[l].b; }
   dim3 grid(const MgLevel& Lv) const { return stencil_grid(Lv.nx, Lv.ny, Lv.nz, h.S, DIM); }
@@ -501,7 +513,8 @@ struct MgRunner {
     else
       k_mg_smooth<DIM><<<grid(Lv), block(), 0, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, from_zero ? 1 : 0,
                                                     h.d_active);
-    hook->after(kKMgSmooth, s, n8 * (from_zero ? 2 : 3));
+    hook->after(kKMgSmooth, s, 0.0);
+    charge(kKMgSmooth, n8 * (from_zero ? 2 : 3), chk);
     std::swap(Lv.x, Lv.t);
     if (chk) {
       check_next = false;
@@ -521,11 +534,13 @@ struct MgRunner {
     hook->before(kKMgRestrict, s);
     k_mg_restrict<DIM><<<grid(Cl), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.nx, Lv.ny, Lv.nz, Cl.b, Cl.nx, Cl.ny,
                                                       Cl.nz, h.d_active);
-    hook->after(kKMgRestrict, s, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell));
+    hook->after(kKMgRestrict, s, 0.0);
+    charge(kKMgRestrict, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell), false);
     vcycle(l + 1);
     hook->before(kKMgProlong, s);
     k_mg_prolong<DIM><<<grid(Lv), block(), 0, s>>>(Lv.x, Lv.nx, Lv.ny, Lv.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
-    hook->after(kKMgProlong, s, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell));
+    hook->after(kKMgProlong, s, 0.0);
+    charge(kKMgProlong, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell), false);
     for (int it = 0; it < d.mg_post; ++it) smooth(l, false);
   }
 };
@@ -579,7 +594,8 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
           R.C[0], x_check, rhs, nullptr, L0.nx, L0.ny, L0.nz, kZChunk, h.d_active, h.d_rmax, nullptr);
     else
       k_mg_resmax<DIM><<<rg, rb, 0, s>>>(R.C[0], x_check, rhs, L0.nx, L0.ny, L0.nz, h.d_active, h.d_rmax, bmax);
-    hook->after(kKMgNorm, s, (x_check == rhs ? 8.0 : 16.0) * n);
+    hook->after(kKMgNorm, s, 0.0);
+    if (R.recording || x_check == rhs) R.fs_bytes = (x_check == rhs ? 8.0 : 16.0) * n;
     x_check = L0.x;
     R.update();
   };
@@ -593,7 +609,9 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     for (;;) {
       for (int b = 0; b < batch && launched <= d.mg_max_cycles; ++b, ++launched) {
         R.check_next = true;
+        R.recording = launched == 0;
         R.vcycle(0);
+        R.recording = false;
       }
       cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
       if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
@@ -604,8 +622,10 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     check();
     for (;;) {
       for (int b = 0; b < batch && launched < d.mg_max_cycles; ++b, ++launched) {
+        R.recording = launched == 0;
         R.vcycle(0);
         check();
+        R.recording = false;
       }
       cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
       if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
@@ -619,6 +639,26 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     cudaMemcpy(cyc.data(), h.d_cycles, sizeof(int) * g.S, cudaMemcpyDeviceToHost);
     int used = 0;
     for (int v : cyc) used = std::max(used, v);
+    // exact compulsory bytes: species s ran c_s full cycles and c_s + 1 checks; unswept species
+    // are copied (2 fields of one species)
+    double checks = 0.0, cycles = 0.0, unswept = 0.0;
+    for (int v : cyc) {
+      checks += v + 1;
+      cycles += v;
+      unswept += v == 0;
+    }
+    const double per = 1.0 / g.S;
+    if (fused) {
+      // the first check sweeps x = b (rhs read once + the partner written), later ones 3 fields
+      const double n8 = 8.0 * (double)n;
+      hook->add_bytes(kKMgSmooth, (2.0 * n8 * g.S + 3.0 * n8 * cycles) * per);
+    } else {
+      hook->add_bytes(kKMgNorm, (8.0 * n * g.S + 16.0 * n * cycles) * per);
+    }
+    (void)checks;
+    for (int c = 0; c < kNumKernelClasses; ++c)
+      if (R.rest_bytes[c] > 0.0) hook->add_bytes(c, R.rest_bytes[c] * cycles * per);
+    hook->add_bytes(kKMgNorm, 16.0 * (double)g.ncell * unswept);
     used = std::max(used, 1);
     bool found = false;
     for (auto& pc : h.predicted)
