@@ -16,6 +16,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include <vector>
 
@@ -286,6 +287,44 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
   if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
 }
 
+// The same level-0 sweep / check with two x-adjacent cells per thread (even nx; walk_pair): 128-bit
+// shared loads of the staged tiles, the rhs staged as pairs; per cell the identical expression.
+// Dynamic shared memory: kPairSmem + kPairAuxSmem.
+template <bool SMOOTH, bool NORM, bool BMAX>
+__global__ void __launch_bounds__(kTX* kTY, 2) k_mg3_pair(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+                                                          const double* __restrict__ b, double* __restrict__ xo, int nx,
+                                                          int ny, int nz, int kc, const int* __restrict__ active,
+                                                          double* __restrict__ out, double* __restrict__ bmax) {
+  extern __shared__ __align__(16) double mg_pring[];
+  __shared__ double red[kTX * kTY / 32];
+  __shared__ double redb[kTX * kTY / 32];
+  const ZChunk z = zchunk(nz, kc);
+  if (!active[z.s]) return;  // uniform per block
+  const long long ncell = (long long)nx * ny * nz;
+  const long long sbase = (long long)z.s * ncell;
+  double* xos = SMOOTH ? opaque(xo + sbase) : nullptr;
+  const int s = z.s;
+  const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
+  double m = 0.0, mb = 0.0;
+  walk_pair<true>(x + sbase, b + sbase, nx, ny, nz, z, mg_pring, mg_pring + kRing * kPPlaneSlot, [](int) {},
+                  [&](int, unsigned cell, const PairTaps& v, const double (&bv)[2], bool ok) {
+                    double xn[2];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                      double lap = 0.0;
+                      lap = lap + cs0 * (-v.x[c] + 16.0 * v.x[c + 1] - 30.0 * v.x[c + 2] + 16.0 * v.x[c + 3] - v.x[c + 4]);
+                      lap = lap + cs1 * (-v.y[c][0] + 16.0 * v.y[c][1] - 30.0 * v.y[c][2] + 16.0 * v.y[c][3] - v.y[c][4]);
+                      lap = lap + cs2 * (-v.z[c][0] + 16.0 * v.z[c][1] - 30.0 * v.z[c][2] + 16.0 * v.z[c][3] - v.z[c][4]);
+                      const double r = bv[c] - (v.x[c + 2] - coef * lap);
+                      xn[c] = v.z[c][2] + wd * r;
+                      if (NORM) m = max_keep(m, ok ? fabs(r) : 0.0);
+                      if (BMAX) mb = max_keep(mb, ok ? fabs(bv[c]) : 0.0);
+                    }
+                    if (SMOOTH && ok) __stcg(reinterpret_cast<double2*>(xos + cell), make_double2(xn[0], xn[1]));
+                  });
+  if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
+}
+
 // launched on the COARSE grid
 template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_restrict(const __grid_constant__ MgCoef C, const double* __restrict__ x,
@@ -446,6 +485,22 @@ inline int mg_plan(const MgHierarchy& h, const cisdc_problem_desc& d, double coe
   return L;
 }
 
+// two cells per thread for the level-0 sweeps on even-nx 3-D grids (CISDC_MG_PAIR=0: one per thread)
+inline bool mg_pair_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_MG_PAIR");
+    if (e && e[0] == '0') return false;
+    const int sm = (int)(kPairSmem + kPairAuxSmem);
+    return cudaFuncSetAttribute(k_mg3_pair<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_mg3_pair<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_mg3_pair<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess;
+  }();
+  return v;
+}
+
 template <int DIM>
 struct MgRunner {
   MgHierarchy& h;
@@ -493,9 +548,22 @@ struct MgRunner {
     const bool chk = l == 0 && check_next;
     const bool bm = chk && first_check;
     const bool tiled = DIM == 3 && !from_zero && tile3d_ok(Lv.ncell);
+    const bool pair = tiled && Lv.nx % 2 == 0 && mg_pair_enabled();
     const double n8 = 8.0 * Lv.ncell * h.S;
     hook->before(kKMgSmooth, s);  // a checking sweep is still a sweep (its norm is a by-product)
-    if (tiled && bm)
+    if (pair) {
+      const dim3 pg = tile3d_pair_grid(Lv.nx, Lv.ny, Lv.nz, h.S);
+      const size_t sm = kPairSmem + kPairAuxSmem;
+      if (bm)
+        k_mg3_pair<true, true, true><<<pg, dim3(kTX, kTY), sm, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz,
+                                                                     kZChunk, h.d_active, h.d_rmax, h.d_bmax);
+      else if (chk)
+        k_mg3_pair<true, true, false><<<pg, dim3(kTX, kTY), sm, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz,
+                                                                      kZChunk, h.d_active, h.d_rmax, nullptr);
+      else
+        k_mg3_pair<true, false, false><<<pg, dim3(kTX, kTY), sm, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz,
+                                                                       kZChunk, h.d_active, nullptr, nullptr);
+    } else if (tiled && bm)
       k_mg3_tiled<true, true, true><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
           C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, h.d_rmax, h.d_bmax);
     else if (tiled && chk)

@@ -298,9 +298,14 @@ struct PairTaps {
   double z[2][5];
 };
 
-template <class PlaneFn, class Body>
-__device__ __forceinline__ void walk_pair(const double* __restrict__ f, int nx, int ny, int nz, const ZChunk& z,
-                                          double* ring, PlaneFn plane, Body body) {
+constexpr size_t kPairAuxSmem = (size_t)kRing * kTX * kTY * 2 * sizeof(double);  // 32 KB
+
+// HAS_AUX: a pointwise field (the multigrid rhs) staged as pairs in aux_ring (kRing x 512 doubles);
+// body(k, cell, taps, aux_pair[2], ok).
+template <bool HAS_AUX, class PlaneFn, class Body>
+__device__ __forceinline__ void walk_pair(const double* __restrict__ f, const double* __restrict__ aux, int nx,
+                                          int ny, int nz, const ZChunk& z, double* ring, double* aux_ring,
+                                          PlaneFn plane, Body body) {
   const int i0 = blockIdx.x * kPTX, j0 = blockIdx.y * kTY;
   const int i = i0 + 2 * threadIdx.x, j = j0 + threadIdx.y;
   const int t = threadIdx.y * kTX + threadIdx.x;
@@ -324,6 +329,8 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, int nx, 
     }
   }
   const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+  const unsigned aux_s = HAS_AUX ? (unsigned)__cvta_generic_to_shared(aux_ring + 2 * t) : 0u;
+  if (HAS_AUX) aux = opaque(aux);
   auto issue = [&](int kk) {
     if (kk <= z.k1 + 1) {
       const double* fp = opaque(f + (unsigned)wrapi(kk, nz) * pl);
@@ -331,6 +338,8 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, int nx, 
 #pragma unroll
       for (int u = 0; u < kPChunkPer; ++u)
         if ((u + 1) * kTX * kTY <= kPChunks || slot[u] >= 0) cp_async16(sb + (unsigned)slot[u] * 8u, fp + off[u]);
+      if (HAS_AUX && kk >= z.k0 && kk < z.k1)
+        cp_async16(aux_s + (unsigned)((kk & (kRing - 1)) * kTX * kTY * 2) * 8u, aux + (unsigned)kk * pl + col);
     }
     cp_async_commit();
   };
@@ -366,7 +375,9 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, int nx, 
       v.z[0][o] = q[0][(P + o) % 5];
       v.z[1][o] = q[1][(P + o) % 5];
     }
-    body(k, (unsigned)k * pl + col, v, in);
+    double av[2] = {0.0, 0.0};
+    if (HAS_AUX) ld2(aux_ring + (k & (kRing - 1)) * kTX * kTY * 2 + 2 * t, av[0], av[1]);
+    body(k, (unsigned)k * pl + col, v, av, in);
   };
   cp_async_wait<3>();
   __syncthreads();
@@ -424,8 +435,8 @@ __global__ void __launch_bounds__(kTX* kTY, 2) k_eval_ad3_pair(Ops o, Geom g, co
   double t2r[3], t2l[3];
   double fz_carry[2] = {0.0, 0.0};
   int carry_k = -1;
-  walk_pair(
-      phi + sbase, g.nx, g.ny, g.nz, z, pring,
+  walk_pair<false>(
+      phi + sbase, nullptr, g.nx, g.ny, g.nz, z, pring, nullptr,
       [&](int k) {
         if (UCONST) return;
 #pragma unroll
@@ -434,7 +445,7 @@ __global__ void __launch_bounds__(kTX* kTY, 2) k_eval_ad3_pair(Ops o, Geom g, co
           t2l[a] = t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0;
         }
       },
-      [&](int k, unsigned cell, const PairTaps& v, bool ok) {
+      [&](int k, unsigned cell, const PairTaps& v, const double (&)[2], bool ok) {
         // per-cell 5-tap views: x taps of cell c are v.x[c .. c+4]
         if (fas) {
           double acc[2] = {0.0, 0.0};
