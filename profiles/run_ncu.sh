@@ -20,7 +20,7 @@ cap() {  # name regex count
   $N -i $rep.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_${CFG}_$1_source.csv 2>/dev/null
   gzip -f gpurun_out/${TAG}_${CFG}_$1_source.csv
 }
-cap mg3 k_mg3_tiled 4
+cap mg3 "k_mg3_tiled|k_mg3_pair" 4
 cap eval k_eval_ad3 2
 cap react "^k_react$" 2
 cap rhs "k_rhs|k_quad|k_mg_update|copy_unswept" 4
