@@ -168,12 +168,24 @@ def cpu_reference_sample(cfg_name: str, scheme: int, workers: int, steps: int | 
     return updates / dt, dt, sample, "reference" if have_ref else "port", max(1, workers if workers > 0 else 1)
 
 
+def workload_config(cfg_name: str, spec, scheme: int, workers: int, scale: int = 1) -> dict:
+    """The bench line's config object (shared by both arms).  `spec` may be a scaled sample of the
+    workload: its per-axis scale is multiplied back."""
+    desc = spec.problem
+    n = [x * scale for x in desc.n[: desc.ndim]]
+    dofs = int(np.prod(n)) * desc.nspecies
+    return {"workload": f"{cfg_name}: {desc.name} {'x'.join(map(str, n))} x {desc.nspecies} species",
+            "scheme": ["misdc", "misdcq", "cisdcq"][scheme], "nu": spec.nu, "workers": workers, "M": spec.M,
+            "sweeps_per_step": spec.n_sweeps, "dt": spec.dt, "dofs": dofs, "updates_per_step": dofs * spec.M * spec.n_sweeps,
+            "l2": "inputs larger than L2 (each field %.2f GB)" % (8 * dofs / 1e9)}
+
+
 def run_reference_arm(args, ws, rank):
     if rank != 0:
         return
     from paper_1801_01201_b200 import problems
-    spec = problems.CONFIGS[args.config](scale=CPU_SAMPLE.get(args.config, (8, 1))[0]) if args.config != "c0" \
-        else problems.config_c0()
+    sample_scale = CPU_SAMPLE.get(args.config, (8, 1))[0] if args.config != "c0" else 1
+    spec = problems.CONFIGS[args.config](scale=sample_scale) if args.config != "c0" else problems.config_c0()
     scheme = spec.scheme if args.scheme is None else args.scheme
     nproc = os.cpu_count() or 1
     workers = min(nproc, max(2 * spec.nu, spec.M)) if scheme == 2 else 0
@@ -193,7 +205,8 @@ def run_reference_arm(args, ws, rank):
         "unit": "updates/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded BASELINE config generator)",
-        "config": {"workload": f"{args.config} (bounded CPU sample)", "scheme": scheme, "workers": workers},
+        "config": dict(workload_config(args.config, spec, scheme, 2 if scheme == 2 else 0, sample_scale),
+                       parallelism=f"replicas x{args.gpus}"),
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -342,12 +355,8 @@ def main():
             "value": value, "unit": "updates/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": tmax / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded BASELINE config generator, problems.py)",
-            "config": {"workload": f"{args.config}: {spec.problem.name} {'x'.join(map(str, desc.n[:desc.ndim]))} "
-                                   f"x {desc.nspecies} species", "scheme": ["misdc", "misdcq", "cisdcq"][scheme],
-                       "nu": spec.nu, "workers": workers, "M": spec.M, "sweeps_per_step": spec.n_sweeps,
-                       "dt": spec.dt, "dofs": n, "updates_per_step": updates_per_step,
-                       "l2": "inputs larger than L2 (each field %.2f GB)" % (8 * n / 1e9),
-                       "parallelism": f"replicas x{ws}"},
+            "config": dict(workload_config(args.config, spec, scheme, workers),
+                           parallelism=f"replicas x{ws}"),
             "e2e": {"value": e2e_value, "unit": "updates/s", "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n,
                     "ms_per_step": e2e_ms / args.steps, "wall_s": wall},
             "gpu_launches": launches,
