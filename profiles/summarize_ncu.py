@@ -114,7 +114,7 @@ def main():
                                 "dram_pct": r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                                 "fp64_pipe_pct": r.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                                 "l1_pct": r.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
-                                "source": f"profiles/{tag}/{tag}_{cfg}_{part}_raw.csv (first captured launch)"}
+                                "source": f"profiles/r1/{tag}_{cfg}_{part}_raw.csv (first captured launch)"}
     lines.append("")
     with open(os.path.join(here, f"{tag}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
