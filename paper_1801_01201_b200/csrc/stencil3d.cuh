@@ -399,7 +399,7 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, const do
 
 // F_A and/or F_D, 3-D periodic, two cells per thread (nx even); UCONST as k_eval_ad3_tiled.
 template <bool UCONST>
-__global__ void __launch_bounds__(kTX* kTY, 2) k_eval_ad3_pair(Ops o, Geom g, const double* __restrict__ phi,
+__global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_pair(Ops o, Geom g, const double* __restrict__ phi,
                                                                double* __restrict__ fa, double* __restrict__ fd, int kc) {
   extern __shared__ __align__(16) double pring[];
   const ZChunk z = zchunk(g.nz, kc);
