@@ -289,9 +289,9 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
 
 // The same level-0 sweep / check with two x-adjacent cells per thread (even nx; walk_pair): 128-bit
 // shared loads of the staged tiles, the rhs staged as pairs; per cell the identical expression.
-// Dynamic shared memory: kPairSmem + kPairAuxSmem.
+// Dynamic shared memory: kMgPairSmem (6-plane rings, 3 blocks per SM).
 template <bool SMOOTH, bool NORM, bool BMAX>
-__global__ void __launch_bounds__(kTX* kTY, 2) k_mg3_pair(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+__global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_pair(const __grid_constant__ MgCoef C, const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ xo, int nx,
                                                           int ny, int nz, int kc, const int* __restrict__ active,
                                                           double* __restrict__ out, double* __restrict__ bmax) {
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kTX* kTY, 2) k_mg3_pair(const __grid_constant_
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_pair<true>(x + sbase, b + sbase, nx, ny, nz, z, mg_pring, mg_pring + kRing * kPPlaneSlot, [](int) {},
+  walk_pair<true, kMgRing>(x + sbase, b + sbase, nx, ny, nz, z, mg_pring, mg_pring + kMgRing * kPPlaneSlot, [](int) {},
                   [&](int, unsigned cell, const PairTaps& v, const double (&bv)[2], bool ok) {
                     double xn[2];
 #pragma unroll
@@ -490,7 +490,7 @@ inline bool mg_pair_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("CISDC_MG_PAIR");
     if (e && e[0] == '0') return false;
-    const int sm = (int)(kPairSmem + kPairAuxSmem);
+    const int sm = (int)kMgPairSmem;
     return cudaFuncSetAttribute(k_mg3_pair<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
                cudaSuccess &&
            cudaFuncSetAttribute(k_mg3_pair<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
@@ -553,7 +553,7 @@ struct MgRunner {
     hook->before(kKMgSmooth, s);  // a checking sweep is still a sweep (its norm is a by-product)
     if (pair) {
       const dim3 pg = tile3d_pair_grid(Lv.nx, Lv.ny, Lv.nz, h.S);
-      const size_t sm = kPairSmem + kPairAuxSmem;
+      const size_t sm = kMgPairSmem;
       if (bm)
         k_mg3_pair<true, true, true><<<pg, dim3(kTX, kTY), sm, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, Lv.nz,
                                                                      kZChunk, h.d_active, h.d_rmax, h.d_bmax);

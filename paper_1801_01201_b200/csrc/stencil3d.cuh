@@ -299,13 +299,29 @@ struct PairTaps {
 };
 
 constexpr size_t kPairAuxSmem = (size_t)kRing * kTX * kTY * 2 * sizeof(double);  // 32 KB
+// the multigrid sweep's smaller rings (6 planes each: 39 + 24 KB) fit 3 blocks per SM
+constexpr int kMgRing = 6;
+constexpr size_t kMgPairSmem = (size_t)kMgRing * (kPPlaneSlot + kTX * kTY * 2) * sizeof(double);
 
 // HAS_AUX: a pointwise field (the multigrid rhs) staged as pairs in aux_ring (kRing x 512 doubles);
 // body(k, cell, taps, aux_pair[2], ok).
-template <bool HAS_AUX, class PlaneFn, class Body>
+// RING: plane slots (>= 6: planes k .. k+5 are live; 8 uses a mask, others a modulo).
+template <int RING>
+__device__ __forceinline__ int ring_slot(int kk) {
+  if constexpr ((RING & (RING - 1)) == 0) return kk & (RING - 1);
+  const int r = kk % RING;
+  return r < 0 ? r + RING : r;
+}
+
+template <bool HAS_AUX, int RING, class PlaneFn, class Body>
 __device__ __forceinline__ void walk_pair(const double* __restrict__ f, const double* __restrict__ aux, int nx,
                                           int ny, int nz, const ZChunk& z, double* ring, double* aux_ring,
                                           PlaneFn plane, Body body) {
+  // AHEAD planes are staged ahead of the one being computed: the prologue stages k0-2 .. k0+AHEAD-1
+  // (all of them must fit, since the queue is filled from k0-2 .. k0+1 before the first step), the
+  // step of plane k stages k+AHEAD into the slot of plane k+AHEAD-RING (dead).
+  constexpr int AHEAD = RING - 2;
+  static_assert(AHEAD >= 4, "the queue needs plane k+2 while k+3 is in flight");
   const int i0 = blockIdx.x * kPTX, j0 = blockIdx.y * kTY;
   const int i = i0 + 2 * threadIdx.x, j = j0 + threadIdx.y;
   const int t = threadIdx.y * kTX + threadIdx.x;
@@ -334,17 +350,17 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, const do
   auto issue = [&](int kk) {
     if (kk <= z.k1 + 1) {
       const double* fp = opaque(f + (unsigned)wrapi(kk, nz) * pl);
-      const unsigned sb = ring_s + (unsigned)((kk & (kRing - 1)) * kPPlaneSlot) * 8u;
+      const unsigned sb = ring_s + (unsigned)(ring_slot<RING>(kk) * kPPlaneSlot) * 8u;
 #pragma unroll
       for (int u = 0; u < kPChunkPer; ++u)
         if ((u + 1) * kTX * kTY <= kPChunks || slot[u] >= 0) cp_async16(sb + (unsigned)slot[u] * 8u, fp + off[u]);
       if (HAS_AUX && kk >= z.k0 && kk < z.k1)
-        cp_async16(aux_s + (unsigned)((kk & (kRing - 1)) * kTX * kTY * 2) * 8u, aux + (unsigned)kk * pl + col);
+        cp_async16(aux_s + (unsigned)(ring_slot<RING>(kk) * kTX * kTY * 2) * 8u, aux + (unsigned)kk * pl + col);
     }
     cp_async_commit();
   };
 #pragma unroll
-  for (int kk = -2; kk <= 4; ++kk) issue(z.k0 + kk);
+  for (int kk = -2; kk < AHEAD; ++kk) issue(z.k0 + kk);
   const int cidx = (threadIdx.y + kHalo) * kPTileP + 2 * threadIdx.x + kHalo;  // cell i in the tile
   double q[2][5];
   auto ld2 = [&](const double* p, double& a, double& b) {
@@ -354,11 +370,11 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, const do
   };
   auto step = [&](auto ph, int k) {
     constexpr int P = decltype(ph)::value;
-    cp_async_wait<2>();
+    cp_async_wait<AHEAD - 3>();  // plane k+2 has landed
     __syncthreads();
-    issue(k + 5);
-    const double* tk = ring + (k & (kRing - 1)) * kPPlaneSlot;
-    ld2(ring + ((k + 2) & (kRing - 1)) * kPPlaneSlot + cidx, q[0][(P + 4) % 5], q[1][(P + 4) % 5]);
+    issue(k + AHEAD);
+    const double* tk = ring + ring_slot<RING>(k) * kPPlaneSlot;
+    ld2(ring + ring_slot<RING>(k + 2) * kPPlaneSlot + cidx, q[0][(P + 4) % 5], q[1][(P + 4) % 5]);
     plane(k);
     PairTaps v;
     ld2(tk + cidx - 2, v.x[0], v.x[1]);
@@ -376,13 +392,13 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, const do
       v.z[1][o] = q[1][(P + o) % 5];
     }
     double av[2] = {0.0, 0.0};
-    if (HAS_AUX) ld2(aux_ring + (k & (kRing - 1)) * kTX * kTY * 2 + 2 * t, av[0], av[1]);
+    if (HAS_AUX) ld2(aux_ring + ring_slot<RING>(k) * kTX * kTY * 2 + 2 * t, av[0], av[1]);
     body(k, (unsigned)k * pl + col, v, av, in);
   };
-  cp_async_wait<3>();
+  cp_async_wait<AHEAD - 2>();  // planes k0-2 .. k0+1
   __syncthreads();
 #pragma unroll
-  for (int o = 0; o < 4; ++o) ld2(ring + ((z.k0 + o - 2) & (kRing - 1)) * kPPlaneSlot + cidx, q[0][o], q[1][o]);
+  for (int o = 0; o < 4; ++o) ld2(ring + ring_slot<RING>(z.k0 + o - 2) * kPPlaneSlot + cidx, q[0][o], q[1][o]);
   for (int k = z.k0; k < z.k1; k += 5) {
     step(Phase<0>{}, k);
     if (k + 1 >= z.k1) break;
@@ -435,7 +451,7 @@ __global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_pair(Ops 
   double t2r[3], t2l[3];
   double fz_carry[2] = {0.0, 0.0};
   int carry_k = -1;
-  walk_pair<false>(
+  walk_pair<false, kRing>(
       phi + sbase, nullptr, g.nx, g.ny, g.nz, z, pring, nullptr,
       [&](int k) {
         if (UCONST) return;
