@@ -1,6 +1,6 @@
 #!/bin/bash
 # ncu recipe for the profiles/ summaries (run on the GPU box from the repo root, one GPU):
-#   bash profiles/run_ncu.sh <tag> [config] [scale]
+#   bash profiles/run_ncu.sh <tag> [config] [scale] [hot|all] [launches]
 # 1. launch list (serialised per-launch durations) of one SDC step through the C-ABI
 # 2. --set full captures of the hot kernels, exported on the box to CSV (raw metrics, details,
 #    source) so that only small files travel back
@@ -20,8 +20,13 @@ cap() {  # name regex count
   $N -i $rep.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_${CFG}_$1_source.csv 2>/dev/null
   gzip -f gpurun_out/${TAG}_${CFG}_$1_source.csv
 }
-cap mg3 "k_mg3_tiled|k_mg3_pair" 4
-cap eval k_eval_ad3 2
-cap react "^k_react$" 2
-cap rhs "k_rhs|k_quad|k_mg_update|copy_unswept" 4
+if [ "${4:-hot}" = "all" ]; then
+  # every kernel class of a (small) config: the first ${5:-60} launches, one capture
+  cap all ".*" ${5:-60}
+else
+  cap mg3 "k_mg3_tiled|k_mg3_pair" 4
+  cap eval k_eval_ad3 2
+  cap react "^k_react$" 2
+  cap rhs "k_rhs|k_quad|k_mg_update|copy_unswept" 4
+fi
 ls -la gpurun_out
