@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_pair(const __grid_constant_
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_pair<true, kMgRing>(x + sbase, b + sbase, nx, ny, nz, z, mg_pring, mg_pring + kMgRing * kPPlaneSlot, [](int) {},
+  walk_pair<true, kMgRing, kMgRing - 2>(x + sbase, b + sbase, nx, ny, nz, z, mg_pring, mg_pring + kMgRing * kPPlaneSlot, [](int) {},
                   [&](int, unsigned cell, const PairTaps& v, const double (&bv)[2], bool ok) {
                     double xn[2];
 #pragma unroll

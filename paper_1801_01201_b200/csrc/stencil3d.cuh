@@ -313,15 +313,14 @@ __device__ __forceinline__ int ring_slot(int kk) {
   return r < 0 ? r + RING : r;
 }
 
-template <bool HAS_AUX, int RING, class PlaneFn, class Body>
+template <bool HAS_AUX, int RING, int AHEAD, class PlaneFn, class Body>
 __device__ __forceinline__ void walk_pair(const double* __restrict__ f, const double* __restrict__ aux, int nx,
                                           int ny, int nz, const ZChunk& z, double* ring, double* aux_ring,
                                           PlaneFn plane, Body body) {
   // AHEAD planes are staged ahead of the one being computed: the prologue stages k0-2 .. k0+AHEAD-1
   // (all of them must fit, since the queue is filled from k0-2 .. k0+1 before the first step), the
   // step of plane k stages k+AHEAD into the slot of plane k+AHEAD-RING (dead).
-  constexpr int AHEAD = RING - 2;
-  static_assert(AHEAD >= 4, "the queue needs plane k+2 while k+3 is in flight");
+  static_assert(AHEAD >= 4 && AHEAD + 2 <= RING, "ring too small for the staging distance");
   const int i0 = blockIdx.x * kPTX, j0 = blockIdx.y * kTY;
   const int i = i0 + 2 * threadIdx.x, j = j0 + threadIdx.y;
   const int t = threadIdx.y * kTX + threadIdx.x;
@@ -451,7 +450,7 @@ __global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_pair(Ops 
   double t2r[3], t2l[3];
   double fz_carry[2] = {0.0, 0.0};
   int carry_k = -1;
-  walk_pair<false, kRing>(
+  walk_pair<false, kRing, 5>(
       phi + sbase, nullptr, g.nx, g.ny, g.nz, z, pring, nullptr,
       [&](int k) {
         if (UCONST) return;
