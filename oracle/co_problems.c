@@ -597,6 +597,7 @@ static circ_t circ_factor(double c) {
 }
 
 #define SCAN_T 512
+#define SCAN_MAXCL 16 /* CTAs per cluster before the elements per thread grow (circulant.hpp) */
 #define SCAN_NW (SCAN_T / 32)
 
 /* rec_step of solve1d.cuh */
@@ -707,7 +708,7 @@ static void scan_pass(double* u, int N, int E, int CL, int reverse, int kind, do
 static int adr_solve_diffusion_scan(co_problem* p, double coef, const double* rhs, double* out) {
   const int N = p->nx;
   int E = 1;
-  while (E < 32 && (long long)E * SCAN_T * 8 < N) E *= 2;
+  while (E < 32 && (long long)E * SCAN_T * SCAN_MAXCL < N) E *= 2;
   const int CL = (N + E * SCAN_T - 1) / (E * SCAN_T);
   aff_t* ex = (aff_t*)malloc(sizeof(aff_t) * CL * SCAN_T);
   aff_t tot[64];

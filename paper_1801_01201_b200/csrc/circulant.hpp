@@ -75,11 +75,13 @@ inline CircFactor factor_circulant(double c) {
   return f;
 }
 
-// Block decomposition of the scan: T threads per CTA, E elements per thread, CL CTAs per cluster.
+// Block decomposition of the scan: T threads per CTA, E elements per thread, CL CTAs per cluster
+// (up to 16, the non-portable cluster size: more SMs before the per-thread chains grow).
 constexpr int kSolve1dThreads = 512;
+constexpr int kSolve1dMaxCluster = 16;
 inline void solve1d_blocking(int N, int* E, int* CL) {
   int e = 1;
-  while (e < 32 && (long long)e * kSolve1dThreads * 8 < N) e *= 2;
+  while (e < 32 && (long long)e * kSolve1dThreads * kSolve1dMaxCluster < N) e *= 2;
   *E = e;
   *CL = (N + e * kSolve1dThreads - 1) / (e * kSolve1dThreads);
 }

@@ -466,6 +466,13 @@ int launch_solve1d_e(cisdc_gpu_ctx* ctx, const Solve1dArgs& a, int cl, cudaStrea
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (cl > 8) {
+    static bool np = false;  // per instance: clusters above 8 CTAs are opt-in
+    if (!np) {
+      CU(cudaFuncSetAttribute(k_solve1d_periodic<E, T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      np = true;
+    }
+  }
   ctx->tm.before(kKSolve1d, s);
   CU(cudaLaunchKernelEx(&cfg, k_solve1d_periodic<E, T>, a));
   ctx->tm.after(kKSolve1d, s, 2.0 * F8(ctx));
