@@ -91,7 +91,13 @@ def main():
         p = os.path.join(d, f"{tag}_{cfg}_{part}_raw.csv")
         if not os.path.exists(p):
             continue
+        seen = set()
         for r in load_raw(p):
+            if part == "all":  # one row per distinct kernel (its first capture)
+                key = r["kernel"].split("(")[0]
+                if key in seen:
+                    continue
+                seen.add(key)
             t = r.get("gpu__time_duration.sum", 0.0)
             rd, wr = r.get("dram__bytes_read.sum", 0.0), r.get("dram__bytes_write.sum", 0.0)
             cells = []
@@ -116,7 +122,8 @@ def main():
                                 "l1_pct": r.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
                                 "source": f"profiles/r1/{tag}_{cfg}_{part}_raw.csv (first captured launch)"}
     lines.append("")
-    with open(os.path.join(here, f"{tag}_summary.md"), "w") as f:
+    name = f"{tag}_summary.md" if cfg == "c5" else f"{tag}_{cfg}_summary.md"
+    with open(os.path.join(here, name), "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(os.path.join(here, f"ncu_traffic_{cfg}.json"), "w") as f:
         json.dump({k: v for k, v in traffic.items()}, f, indent=1)
