@@ -10,7 +10,7 @@ CFG=${2:-c5}
 SCALE=${3:-1}
 N=/usr/local/cuda/bin/ncu
 mkdir -p gpurun_out
-STEP="python tests/profile_step.py --config $CFG --scale $SCALE"
+STEP="python tools/profile_step.py --config $CFG --scale $SCALE"
 $N --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv $STEP > gpurun_out/ncu_${TAG}_l.log 2>&1
 cap() {  # name regex count
   local rep=/tmp/${TAG}_${CFG}_$1

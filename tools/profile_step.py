@@ -1,6 +1,6 @@
 """One SDC time step of a config through the C-ABI (device-resident), for ncu captures.
 
-  python tests/profile_step.py --config c5 --scale 2 [--steps 1]
+  python tools/profile_step.py --config c5 --scale 2 [--steps 1]
 """
 import argparse
 import ctypes as C
