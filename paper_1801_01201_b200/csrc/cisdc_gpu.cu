@@ -75,6 +75,8 @@ struct Timing final : LaunchHook {
     cudaEventRecord(cur, s);
   }
   void add_bytes(int cls, double b) override { bytes[cls] += b; }
+  void add_launches(long long n) override { launches += n; }
+  bool timing() const override { return on; }
   void after(int cls, cudaStream_t s, double b) override {
     ++launches;
     ++count[cls];

@@ -75,6 +75,10 @@ struct LaunchHook {
   virtual void after(int cls, cudaStream_t s, double bytes) = 0;
   // bytes known only after the fact (multigrid: per-species masking decided on the device)
   virtual void add_bytes(int, double) {}
+  // kernels launched through a CUDA graph replay (counted, not individually timed)
+  virtual void add_launches(long long) {}
+  // per-launch timing active (graph replays are then not used, so every launch is timed)
+  virtual bool timing() const { return false; }
   virtual ~LaunchHook() = default;
 };
 #endif

@@ -47,6 +47,16 @@ struct MgHierarchy {
   int* d_flag = nullptr;          // [2]: any_active, failed species + 1
   int* h_flag = nullptr;          // pinned mirror
   std::vector<std::pair<double, int>> predicted;  // cycles the last solve with this coef needed
+  // Captured V-cycles (the cycles after the first of a solve are identical launch sequences for a
+  // given coefficient and output buffer): one graph launch replaces a cycle's tens of kernels.
+  struct CycleGraph {
+    double coef;
+    const void *rhs, *out;
+    int L;
+    cudaGraphExec_t exec;
+    long long kernels;
+  };
+  std::vector<CycleGraph> graphs;
   std::vector<void*> allocs;
 };
 
@@ -448,6 +458,8 @@ inline int mg_init(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d) {
 }
 
 inline void mg_free(MgHierarchy& h) {
+  for (auto& g : h.graphs) cudaGraphExecDestroy(g.exec);
+  h.graphs.clear();
   for (void* p : h.allocs) cudaFree(p);
   h.allocs.clear();
   if (h.h_flag) cudaFreeHost(h.h_flag);
@@ -500,6 +512,14 @@ inline bool mg_pair_enabled() {
   }();
   return v;
 }
+
+// Wraps the engine's hook while a cycle is captured: counts the kernels (the replays are charged
+// that many launches) and forwards nothing else (no timing events inside a graph).
+struct CountingHook final : LaunchHook {
+  long long n = 0;
+  void before(int, cudaStream_t) override {}
+  void after(int, cudaStream_t, double) override { ++n; }
+};
 
 template <int DIM>
 struct MgRunner {
@@ -613,6 +633,48 @@ struct MgRunner {
   }
 };
 
+inline bool graphs_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_MG_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+// The cached graph of one checking V-cycle (cycles >= 1 of a solve) for (coef, rhs, out, L); built
+// by capturing R.vcycle(0) on the stream.  nullptr if capture is unavailable (the caller then
+// launches the cycle directly).
+template <int DIM>
+inline MgHierarchy::CycleGraph* cycle_graph(MgHierarchy& h, MgRunner<DIM>& R, double coef, const double* rhs,
+                                            const double* out, cudaStream_t s) {
+  for (auto& g : h.graphs)
+    if (g.coef == coef && g.rhs == rhs && g.out == out && g.L == R.L) return &g;
+  CountingHook counter;
+  LaunchHook* saved = R.hook;
+  R.hook = &counter;
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    R.hook = saved;
+    return nullptr;
+  }
+  R.check_next = true;
+  R.recording = false;
+  R.vcycle(0);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(s, &graph);
+  R.hook = saved;
+  if (e != cudaSuccess || !graph) return nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) return nullptr;
+  if (h.graphs.size() >= 64) {
+    cudaGraphExecDestroy(h.graphs.front().exec);
+    h.graphs.erase(h.graphs.begin());
+  }
+  h.graphs.push_back({coef, rhs, out, R.L, exec, counter.n});
+  return &h.graphs.back();
+}
+
 // The oracle's loop per species: x = b; while (||b - A x|| > tol ||b||) { cap check; V-cycle }.
 // Device form: every enqueued V-cycle starts with a level-0 sweep that also reduces the residual
 // norm of its input iterate (k_mg3_tiled<.., NORM> / k_mg_smooth<.., NORM>), followed by the
@@ -672,10 +734,22 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     if (pc.first == coef) batch = std::max(1, pc.second);
   int launched = 0;  // V-cycles enqueued
   if (fused) {
-    // cycle i checks x_{i-1} first: n real cycles need n + 1 enqueued ones
+    // cycle i checks x_{i-1} first: n real cycles need n + 1 enqueued ones.  Cycles after the first
+    // replay a captured graph of the cycle (same kernels, same pointers: the sweep counts per level
+    // are even, so the ping-pong pointers are back in place after every cycle).
     batch += 1;
+    const bool use_graph = !hook->timing() && graphs_enabled();
+    MgHierarchy::CycleGraph* cg = nullptr;
     for (;;) {
       for (int b = 0; b < batch && launched <= d.mg_max_cycles; ++b, ++launched) {
+        if (launched >= 1 && use_graph) {
+          if (!cg) cg = cycle_graph(h, R, coef, rhs, out, s);
+          if (cg) {
+            if (cudaGraphLaunch(cg->exec, s) != cudaSuccess) return CISDC_E_CUDA;
+            hook->add_launches(cg->kernels);
+            continue;
+          }
+        }
         R.check_next = true;
         R.recording = launched == 0;
         R.vcycle(0);
