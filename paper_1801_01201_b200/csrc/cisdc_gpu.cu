@@ -245,7 +245,19 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
   ctx->tm.before(kKEvalAD, s);
   switch (g.ndim) {
     case 1: k_eval_ad<1><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
-    case 2: k_eval_ad<2><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
+    case 2:
+      if (g.nx % 2 == 0 && g.nx >= 64 && tile3d_ok(g.ncell) && eval_pair()) {
+        static bool attr = false;
+        if (!attr) {
+          CU(cudaFuncSetAttribute(k_eval_ad2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
+          attr = true;
+        }
+        const int ch = rows_chunk(g.ncell, g.S);
+        k_eval_ad2_rows<<<rows_grid(g.nx, g.ny, g.S, ch), kRowWarps * 32, kRowSmem, s>>>(ctx->ops, g, phi, fa, fd, ch);
+      } else {
+        k_eval_ad<2><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd);
+      }
+      break;
     default:
       if (!tile3d_ok(g.ncell)) {
         k_eval_ad<3><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd);

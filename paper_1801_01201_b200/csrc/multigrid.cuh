@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "stencil.cuh"
+#include "stencil2d.cuh"
 #include "stencil3d.cuh"
 
 namespace cisdc_b200 {
@@ -335,6 +336,41 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_pair(const __grid_constant_
   if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
 }
 
+// 2-D level sweep / check on the row-streaming walker (stencil2d.cuh; nx even): per cell the
+// expression of k_mg_smooth<2> / mg_ax<2>.  Dynamic shared memory kRowSmem.
+template <bool SMOOTH, bool NORM, bool BMAX>
+__global__ void __launch_bounds__(kRowWarps * 32, 2) k_mg2_rows(const __grid_constant__ MgCoef C, const double* __restrict__ x,
+                                                                const double* __restrict__ b, double* __restrict__ xo,
+                                                                int nx, int ny, int chunk, const int* __restrict__ active,
+                                                                double* __restrict__ out, double* __restrict__ bmax) {
+  extern __shared__ __align__(16) double mg_rsm[];
+  __shared__ double red[kRowWarps], redb[kRowWarps];
+  const int s = blockIdx.z;
+  if (!active[s]) return;  // uniform per block
+  const long long ncell = (long long)nx * ny;
+  const long long sbase = (long long)s * ncell;
+  double* xos = SMOOTH ? opaque(xo + sbase) : nullptr;
+  const double c0 = C.c[s][0], c1 = C.c[s][1], coef = C.coef, wd = C.wD[s];
+  const int j0 = blockIdx.y * chunk, j1 = min(ny, j0 + chunk);
+  double m = 0.0, mb = 0.0;
+  walk_rows<true>(x + sbase, b + sbase, nx, ny, j0, j1, mg_rsm, [](int) {},
+                  [&](int, unsigned cell, const RowTaps& v, const double (&bv)[2], bool ok) {
+                    double xn[2];
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                      double lap = 0.0;
+                      lap = lap + c0 * (-v.x[c] + 16.0 * v.x[c + 1] - 30.0 * v.x[c + 2] + 16.0 * v.x[c + 3] - v.x[c + 4]);
+                      lap = lap + c1 * (-v.y[c][0] + 16.0 * v.y[c][1] - 30.0 * v.y[c][2] + 16.0 * v.y[c][3] - v.y[c][4]);
+                      const double r = bv[c] - (v.x[c + 2] - coef * lap);
+                      xn[c] = v.x[c + 2] + wd * r;
+                      if (NORM) m = max_keep(m, ok ? fabs(r) : 0.0);
+                      if (BMAX) mb = max_keep(mb, ok ? fabs(bv[c]) : 0.0);
+                    }
+                    if (SMOOTH && ok) __stcg(reinterpret_cast<double2*>(xos + cell), make_double2(xn[0], xn[1]));
+                  });
+  if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + s, bmax + s);
+}
+
 // launched on the COARSE grid
 template <int DIM>
 __global__ void __launch_bounds__(256) k_mg_restrict(const __grid_constant__ MgCoef C, const double* __restrict__ x,
@@ -497,6 +533,22 @@ inline int mg_plan(const MgHierarchy& h, const cisdc_problem_desc& d, double coe
   return L;
 }
 
+// row-streaming 2-D sweeps (CISDC_MG_ROWS=0: the per-point kernel)
+inline bool mg_rows_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_MG_ROWS");
+    if (e && e[0] == '0') return false;
+    const int sm = (int)kRowSmem;
+    return cudaFuncSetAttribute(k_mg2_rows<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_mg2_rows<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_mg2_rows<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess;
+  }();
+  return v;
+}
+
 // two cells per thread for the level-0 sweeps on even-nx 3-D grids (CISDC_MG_PAIR=0: one per thread)
 inline bool mg_pair_enabled() {
   static const bool v = [] {
@@ -571,7 +623,21 @@ struct MgRunner {
     const bool pair = tiled && Lv.nx % 2 == 0 && mg_pair_enabled();
     const double n8 = 8.0 * Lv.ncell * h.S;
     hook->before(kKMgSmooth, s);  // a checking sweep is still a sweep (its norm is a by-product)
-    if (pair) {
+    const bool rows2 = DIM == 2 && !from_zero && Lv.nx % 2 == 0 && Lv.nx >= 64 && tile3d_ok(Lv.ncell) &&
+                       mg_rows_enabled();
+    if (rows2) {
+      const int ch = rows_chunk(Lv.ncell, h.S);
+      const dim3 rg = rows_grid(Lv.nx, Lv.ny, h.S, ch);
+      if (bm)
+        k_mg2_rows<true, true, true><<<rg, kRowWarps * 32, kRowSmem, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, ch,
+                                                                            h.d_active, h.d_rmax, h.d_bmax);
+      else if (chk)
+        k_mg2_rows<true, true, false><<<rg, kRowWarps * 32, kRowSmem, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, ch,
+                                                                             h.d_active, h.d_rmax, nullptr);
+      else
+        k_mg2_rows<true, false, false><<<rg, kRowWarps * 32, kRowSmem, s>>>(C[l], xin, bof(l), Lv.t, Lv.nx, Lv.ny, ch,
+                                                                              h.d_active, nullptr, nullptr);
+    } else if (pair) {
       const dim3 pg = tile3d_pair_grid(Lv.nx, Lv.ny, Lv.nz, h.S);
       const size_t sm = kMgPairSmem;
       if (bm)

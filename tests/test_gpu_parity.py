@@ -344,3 +344,23 @@ def test_gpu_schedule_trace_valid(gpu, oracle, nu):
         assert np.array_equal(st.phi(spec.M), piped)
     finally:
         st.ctx.close()
+
+
+# ------------------------------------------------------------------ 2-D row-streaming kernels: ragged grids
+
+@pytest.mark.parametrize("n", [(70, 46), (130, 33), (64, 9), (71, 40)])
+def test_rows_2d_ragged(gpu, oracle, n):
+    """The row-streaming 2-D F_A/F_D and multigrid sweeps (even nx >= 64; odd nx takes the per-point
+    kernels) with the vortex velocity, on grids ragged against the 64-column strips and the row
+    chunks: bitwise equal to the oracle, all three schemes."""
+    reac, prod, k, D = P._c45_network()
+    p = P.ProblemDesc(ndim=2, n=(n[0], n[1], 1), nspecies=9, h=(1.0 / n[0], 1.0 / n[1], 1.0),
+                      vel=P.vortex_tables(n[0], n[1]), diffusivity=D, reaction_kind=_abi.REACTION_MASS_ACTION,
+                      reactants=reac, products=prod, rate_constants=k, newton_tol=1e-12, name="c4-like")
+    P.mg_defaults(p)
+    rng = np.random.default_rng(5)
+    fields = P._normalised_fields(rng, n, 9, 16, 3)
+    spec = P.RunSpec(p, P.to_layout(fields), 1, 4, 4, 1e-5, 1, name="c4-like", schemes=(0, 1, 2))
+    for scheme in (0, 1, 2):
+        _, g, c = per_step_compare(oracle, spec, scheme, 1)
+        assert np.array_equal(g, c)
