@@ -444,6 +444,133 @@ __global__ void __launch_bounds__(256) k_mg_prolong(double* __restrict__ x, int 
   x[id] = x[id] + v;
 }
 
+// The coarse end of a V-cycle in one kernel: levels lc .. L-1 (each at most a few thousand cells)
+// for one species per block, with __syncthreads between the steps instead of a launch per step.
+// Per point the operations of k_mg_smooth / k_mg_restrict / k_mg_prolong, in the order of
+// MgRunner::vcycle; the ping-pong pointers of every level make an even number of swaps, so the
+// host-side assignment is unchanged afterwards.
+constexpr int kMgCoarseThreads = 1024;
+struct MgCoarseArgs {
+  int lc, L, pre, post, coarse;
+  int nx[kMgMaxLevels], ny[kMgMaxLevels], nz[kMgMaxLevels];
+  double *x[kMgMaxLevels], *t[kMgMaxLevels], *b[kMgMaxLevels];
+  MgCoef C[kMgMaxLevels];
+  const int* active;
+};
+
+template <int DIM>
+__global__ void __launch_bounds__(kMgCoarseThreads) k_mg_coarse(const __grid_constant__ MgCoarseArgs A) {
+  const int s = blockIdx.x;
+  if (!A.active[s]) return;
+  // the levels' current (x, t) pointers, swapped after every sweep (block-uniform, in shared memory)
+  __shared__ double* xs[kMgMaxLevels];
+  __shared__ double* ts[kMgMaxLevels];
+  if (threadIdx.x == 0)
+    for (int l = A.lc; l < A.L; ++l) {
+      xs[l] = A.x[l];
+      ts[l] = A.t[l];
+    }
+  __syncthreads();
+  auto sweep = [&](int l, bool from_zero) {
+    const int nx = A.nx[l], ny = A.ny[l], nz = A.nz[l];
+    const int nc = nx * ny * nz;
+    const long long base = (long long)s * nc;
+    const MgCoef& C = A.C[l];
+    double* to = ts[l] + base;
+    const double* xsp = xs[l] + base;
+    const double* bs = A.b[l] + base;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      if (from_zero) {
+        to[c] = C.wD[s] * bs[c];
+      } else {
+        const int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+        const double r = bs[c] - mg_ax<DIM>(C, s, xsp, nx, ny, nz, i, j, k);
+        to[c] = xsp[c] + C.wD[s] * r;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double* tmp = xs[l];
+      xs[l] = ts[l];
+      ts[l] = tmp;
+    }
+    __syncthreads();
+  };
+  for (int l = A.lc; l < A.L - 1; ++l) {
+    for (int it = 0; it < A.pre; ++it) sweep(l, l > 0 && it == 0);
+    // restriction into level l+1 (k_mg_restrict)
+    const int nx = A.nx[l], ny = A.ny[l], nz = A.nz[l];
+    const int cx = A.nx[l + 1], cy = A.ny[l + 1], cz = A.nz[l + 1];
+    const int nf = nx * ny * nz, nc = cx * cy * cz;
+    const double* xsp = xs[l] + (long long)s * nf;
+    const double* bsp = A.b[l] + (long long)s * nf;
+    const double scale = DIM == 1 ? 0.5 : (DIM == 2 ? 0.25 : 0.125);
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      const int I = c % cx, J = (c / cx) % cy, K = c / (cx * cy);
+      double acc = 0.0;
+#pragma unroll
+      for (int dz = 0; dz < (DIM >= 3 ? 2 : 1); ++dz)
+#pragma unroll
+        for (int dy = 0; dy < (DIM >= 2 ? 2 : 1); ++dy)
+#pragma unroll
+          for (int dx = 0; dx < 2; ++dx) {
+            const int i = 2 * I + dx, j = DIM >= 2 ? 2 * J + dy : J, k = DIM >= 3 ? 2 * K + dz : K;
+            const long long id = ((long long)k * ny + j) * nx + i;
+            acc = acc + (bsp[id] - mg_ax<DIM>(A.C[l], s, xsp, nx, ny, nz, i, j, k));
+          }
+      A.b[l + 1][(long long)s * nc + c] = acc * scale;
+    }
+    __syncthreads();
+  }
+  {
+    const int l = A.L - 1;
+    const int ns = A.L == 1 ? A.pre : A.coarse;
+    for (int it = 0; it < ns; ++it) sweep(l, l > 0 && it == 0);
+  }
+  for (int l = A.L - 2; l >= A.lc; --l) {
+    // prolongation of level l+1 into level l (k_mg_prolong)
+    const int nx = A.nx[l], ny = A.ny[l], nz = A.nz[l];
+    const int cx = A.nx[l + 1], cy = A.ny[l + 1], cz = A.nz[l + 1];
+    const int nf = nx * ny * nz;
+    const double* e = xs[l + 1] + (long long)s * cx * cy * cz;
+    double* xl = xs[l] + (long long)s * nf;
+    for (int c = threadIdx.x; c < nf; c += blockDim.x) {
+      const int i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+      const int I = i >> 1, I2 = wrapi((i & 1) ? I + 1 : I - 1, cx);
+      int J = j, J2 = j, K = k, K2 = k;
+      if (DIM >= 2) {
+        J = j >> 1;
+        J2 = wrapi((j & 1) ? J + 1 : J - 1, cy);
+      }
+      if (DIM >= 3) {
+        K = k >> 1;
+        K2 = wrapi((k & 1) ? K + 1 : K - 1, cz);
+      }
+#define E_(a, b_, c_) e[((long long)(c_) * cy + (b_)) * cx + (a)]
+      double v;
+      if (DIM == 1) {
+        v = 0.75 * E_(I, 0, 0) + 0.25 * E_(I2, 0, 0);
+      } else if (DIM == 2) {
+        const double a0 = 0.75 * E_(I, J, 0) + 0.25 * E_(I2, J, 0);
+        const double a1 = 0.75 * E_(I, J2, 0) + 0.25 * E_(I2, J2, 0);
+        v = 0.75 * a0 + 0.25 * a1;
+      } else {
+        const double a00 = 0.75 * E_(I, J, K) + 0.25 * E_(I2, J, K);
+        const double a10 = 0.75 * E_(I, J2, K) + 0.25 * E_(I2, J2, K);
+        const double a01 = 0.75 * E_(I, J, K2) + 0.25 * E_(I2, J, K2);
+        const double a11 = 0.75 * E_(I, J2, K2) + 0.25 * E_(I2, J2, K2);
+        const double b0 = 0.75 * a00 + 0.25 * a10;
+        const double b1 = 0.75 * a01 + 0.25 * a11;
+        v = 0.75 * b0 + 0.25 * b1;
+      }
+#undef E_
+      xl[c] = xl[c] + v;
+    }
+    __syncthreads();
+    for (int it = 0; it < A.post; ++it) sweep(l, false);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 
 inline int mg_init(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d) {
@@ -531,6 +658,16 @@ inline int mg_plan(const MgHierarchy& h, const cisdc_problem_desc& d, double coe
   for (int l = 0; l < L; ++l)
     for (int s = 0; s < d.nspecies; ++s) C[l].wD[s] = 2.0 / ((l < L - 1 ? ehf[l][s] : 1.0) + emax[l][s]);
   return L;
+}
+
+// levels of at most this many cells run inside one k_mg_coarse launch (CISDC_MG_COARSE=0: off)
+constexpr long long kMgCoarseCells = 4096;
+inline bool mg_coarse_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_MG_COARSE");
+    return !(e && e[0] == '0');
+  }();
+  return v;
 }
 
 // row-streaming 2-D sweeps (CISDC_MG_ROWS=0: the per-point kernel)
@@ -676,8 +813,31 @@ struct MgRunner {
       update();
     }
   }
+  int lc = kMgMaxLevels;  // first level handled by k_mg_coarse (levels of <= kMgCoarseCells cells)
   void vcycle(int l) {
     MgLevel& Lv = h.lv[l];
+    if (l >= 1 && l >= lc) {  // the rest of the cycle in one launch
+      MgCoarseArgs A{};
+      A.lc = l;
+      A.L = L;
+      A.pre = d.mg_pre;
+      A.post = d.mg_post;
+      A.coarse = d.mg_coarse_sweeps;
+      for (int q = l; q < L; ++q) {
+        A.nx[q] = h.lv[q].nx;
+        A.ny[q] = h.lv[q].ny;
+        A.nz[q] = h.lv[q].nz;
+        A.x[q] = h.lv[q].x;
+        A.t[q] = h.lv[q].t;
+        A.b[q] = h.lv[q].b;
+        A.C[q] = C[q];
+      }
+      A.active = h.d_active;
+      hook->before(kKMgSmooth, s);
+      k_mg_coarse<DIM><<<h.S, kMgCoarseThreads, 0, s>>>(A);
+      hook->after(kKMgSmooth, s, 0.0);
+      return;
+    }
     if (l == L - 1) {
       const int ns = L == 1 ? d.mg_pre : d.mg_coarse_sweeps;
       for (int it = 0; it < ns; ++it) smooth(l, l > 0 && it == 0);
@@ -761,6 +921,12 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   MgRunner<DIM> R{h, d, {}, 1, s, hook, rhs};
   R.st = st;
   R.L = mg_plan(h, d, coef, R.C);
+  if (mg_coarse_enabled())
+    for (int l = 1; l < R.L; ++l)
+      if (h.lv[l].ncell <= kMgCoarseCells) {
+        R.lc = l;
+        break;
+      }
   std::vector<int> ones(g.S, 1);
   cudaMemcpyAsync(h.d_active, ones.data(), sizeof(int) * g.S, cudaMemcpyHostToDevice, s);
   cudaMemsetAsync(h.d_cycles, 0, sizeof(int) * g.S, s);
