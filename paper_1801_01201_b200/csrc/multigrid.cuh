@@ -661,7 +661,7 @@ inline int mg_plan(const MgHierarchy& h, const cisdc_problem_desc& d, double coe
 }
 
 // levels of at most this many cells run inside one k_mg_coarse launch (CISDC_MG_COARSE=0: off)
-constexpr long long kMgCoarseCells = 4096;
+constexpr long long kMgCoarseCells = 1024;
 inline bool mg_coarse_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("CISDC_MG_COARSE");
@@ -922,7 +922,7 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   R.st = st;
   R.L = mg_plan(h, d, coef, R.C);
   if (mg_coarse_enabled())
-    for (int l = 1; l < R.L; ++l)
+    for (int l = 1; l + 1 < R.L; ++l)  // only when it replaces at least two levels
       if (h.lv[l].ncell <= kMgCoarseCells) {
         R.lc = l;
         break;
