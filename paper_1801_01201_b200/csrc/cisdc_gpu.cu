@@ -780,7 +780,9 @@ int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt
   double* out = W.get(0, m, ell);
   TRY(solve_diffusion(ctx, coef, ctx->rhs_d, out, s));
   if (c) ++c->diffusion;
-  if (ell == 1) TRY(launch_eval_ad(ctx, out, ctx->fa_ad[m], ctx->fd_ad[m], s));
+  // fa_ad / fd_ad of slot (m, 1) are read only by D(m+1, 1) (integrators.cpp:215-216): the
+  // reference's evaluation at m = M has no reader and is skipped
+  if (ell == 1 && m < ctx->M) TRY(launch_eval_ad(ctx, out, ctx->fa_ad[m], ctx->fd_ad[m], s));
   return CISDC_OK;
 }
 
