@@ -320,10 +320,13 @@ def main():
     newton_flops = roofline.newton_work(desc, newton, cell_solves, sparse=sparse)
     if dom["kernel"] == "react_newton" and desc.nspecies >= 9:
         achieved = newton_flops / (dom["ms"] * 1e-3) / 1e12
-        roof = {"bound": "fp64", "kernel": dom["kernel"], "achieved": achieved, "peak": pk_fma.value,
-                "unit": "TFLOP/s", "frac": achieved / pk_fma.value,
-                "peak_source": "measured DFMA chain peak on this GPU (cisdc_gpu_fp64_peak)",
-                "peak_dmul_dadd": pk_mul.value, "traffic": None,
+        # The kernel's arithmetic is the reference's no-FMA operation sequence (bit parity), i.e.
+        # DADD / DMUL, one flop per FP64 pipe slot: its attainable peak is the measured DMUL/DADD
+        # issue rate; the DFMA rate (two flops per slot) is listed beside it.
+        roof = {"bound": "fp64", "kernel": dom["kernel"], "achieved": achieved, "peak": pk_mul.value,
+                "unit": "TFLOP/s", "frac": achieved / pk_mul.value,
+                "peak_source": "measured DMUL/DADD chain peak on this GPU (cisdc_gpu_fp64_peak)",
+                "peak_dfma": pk_fma.value, "frac_of_dfma_peak": achieved / pk_fma.value, "traffic": None,
                 "work": f"{newton} Newton trips, analytic {newton_flops:.3e} FP64 flops"}
     else:
         achieved = dom["gbs"]

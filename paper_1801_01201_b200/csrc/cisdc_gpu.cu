@@ -138,6 +138,7 @@ struct cisdc_gpu_ctx {
   double* rd_work = nullptr;
   MgHierarchy mg;
   RtcNewton rtc;  // network-specialised Newton kernels (mass action)
+  bool rtc_pad_set[4] = {};
   unsigned* defer_list = nullptr;  // cells the specialised kernel hands to the dense fixup
   int* defer_count = nullptr;
   // status / reductions
@@ -388,9 +389,20 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t 
     aa.defer_count = ctx->defer_count;
     DevStatus* st = ctx->d_st;
     void* args[5] = {&rx, &o, &g, &aa, &st};
+    // CISDC_REACT_SMEM (bytes, measurement knob): unused dynamic shared memory per block, which caps
+    // the Newton kernel's resident blocks per SM and leaves room for the concurrent D chain's blocks
+    static const int pad = [] {
+      const char* e = std::getenv("CISDC_REACT_SMEM");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (pad > 48 * 1024 && !ctx->rtc_pad_set[mode]) {
+      CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(ctx->rtc.fn[mode]),
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
+      ctx->rtc_pad_set[mode] = true;
+    }
     ctx->tm.before(kKReact, s);
     CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)), dim3(128),
-                        args, 0, s));
+                        args, (size_t)pad, s));
     ctx->tm.after(kKReact, s, F8(ctx) * react_fields(mode, a));
     // cells whose LU needed a row interchange: dense generic kernel, then reset the list
     ctx->tm.before(kKReact, s);
