@@ -455,7 +455,11 @@ int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
   return CISDC_OK;
 }
 
-int launch_quad_base(cisdc_gpu_ctx* ctx, int set, double dt, cudaStream_t s) {
+// quadrature_base for all M rows; fuse (optional): the first stage rhs (k_rhs arguments with
+// nt == 0 and base == base[0]), assembled in the same pass; skip_base0: base row 0 has no other
+// reader and is not stored
+int launch_quad_base(cisdc_gpu_ctx* ctx, int set, double dt, cudaStream_t s, const RhsArgs* fuse = nullptr,
+                     bool skip_base0 = false) {
   QuadArgs q{};
   const int M = ctx->M;
   q.M = M;
@@ -468,11 +472,26 @@ int launch_quad_base(cisdc_gpu_ctx* ctx, int set, double dt, cudaStream_t s) {
     q.fr[j] = V(ctx, set, kFr, j);
   }
   for (int m = 0; m < M; ++m) q.base[m] = ctx->base[m];
-  ctx->tm.before(kKQuad, s);
-  k_quad_base<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(q, ctx->g.n);
   std::vector<const void*> in{q.phi0};
   for (int j = 0; j <= M; ++j) in.insert(in.end(), {q.fa[j], q.fd[j], q.fr[j]});
-  ctx->tm.after(kKQuad, s, F8(ctx) * (distinct_fields(in) + M));
+  double outs = M;
+  if (fuse) {
+    q.rhs0_kind = fuse->kind == kRhsMisdcq ? 1 : 2;
+    q.fc = fuse->fc;
+    q.X = fuse->X;
+    q.Y = fuse->Y;
+    q.Z = fuse->Z;
+    q.rhs0 = fuse->out;
+    in.insert(in.end(), {q.X, q.Y, q.Z});
+    outs += 1;
+    if (skip_base0) {
+      q.base[0] = nullptr;
+      outs -= 1;
+    }
+  }
+  ctx->tm.before(kKQuad, s);
+  k_quad_base<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(q, ctx->g.n);
+  ctx->tm.after(kKQuad, s, F8(ctx) * (distinct_fields(in) + outs));
   CU(cudaGetLastError());
   return CISDC_OK;
 }
@@ -622,7 +641,14 @@ int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
   const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
   cudaStream_t s = ctx->s_main;
   reset_views(ctx, nxt);
-  TRY(launch_quad_base(ctx, prev, dt, s));
+  {  // node 0's diffusion rhs (base - coef fd_p[1]) in the quadrature pass
+    RhsArgs r0{};
+    r0.kind = kRhsMisdcq;
+    r0.fc = dt * QI(ctx->tb, 0, 0);
+    r0.X = V(ctx, prev, kFd, 1);
+    r0.out = ctx->rhs_d;
+    TRY(launch_quad_base(ctx, prev, dt, s, &r0));
+  }
   for (int m = 0; m < M; ++m) {
     const double coef = dt * QI(ctx->tb, m, m);
     RhsArgs r{};
@@ -644,7 +670,7 @@ int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
     r.base = ctx->base[m];
     r.out = ctx->rhs_d;
     r.out2 = m > 0 ? ctx->rhs_r : nullptr;
-    TRY(launch_rhs(ctx, r, s));
+    if (m > 0) TRY(launch_rhs(ctx, r, s));
     TRY(solve_diffusion(ctx, coef, ctx->rhs_d, ctx->phi_ad[m + 1], s));
     if (c) ++c->diffusion;
     ReactArgs a{};
@@ -739,8 +765,8 @@ int ensure_slots(cisdc_gpu_ctx* ctx, int nu) {
   return CISDC_OK;
 }
 
-// cisdcq_cells::run_diffusion_cell (integrators.cpp:195-235)
-int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c) {
+// the right-hand side of run_diffusion_cell (integrators.cpp:201-226) as k_rhs arguments
+RhsArgs diffusion_rhs(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt) {
   const int prev = ctx->cur, row = m - 1;
   RhsArgs r{};
   r.kind = kRhsCisdcq;
@@ -788,7 +814,16 @@ int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt
   r.Z = V(ctx, prev, kFd, m);
   r.base = ctx->base[row];
   r.out = ctx->rhs_d;
-  TRY(launch_rhs(ctx, r, s));
+  return r;
+}
+
+// cisdcq_cells::run_diffusion_cell (integrators.cpp:195-235); rhs_ready: D(1, 1)'s rhs was
+// assembled by the sweep's quadrature pass
+int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c,
+                   bool rhs_ready = false) {
+  const int row = m - 1;
+  const double coef = dt * QI(ctx->tb, row, m - 1);
+  if (!rhs_ready) TRY(launch_rhs(ctx, diffusion_rhs(ctx, W, m, ell, dt), s));
   double* out = W.get(0, m, ell);
   TRY(solve_diffusion(ctx, coef, ctx->rhs_d, out, s));
   if (c) ++c->diffusion;
@@ -827,11 +862,14 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   reset_views(ctx, nxt);
   Slots W{ctx, nxt, nu};
   cudaStream_t sd = ctx->s_main;
-  TRY(launch_quad_base(ctx, ctx->cur, dt, sd));
+  // D(1, 1)'s rhs reads base row 0 and node-1 fields only: assembled by the quadrature pass, and
+  // base row 0 (read by D(1, ell) alone) is then not stored when nu == 1
+  const RhsArgs r11 = diffusion_rhs(ctx, W, 1, 1, dt);
+  TRY(launch_quad_base(ctx, ctx->cur, dt, sd, &r11, nu == 1));
   if (workers <= 0) {
     for (int ell = 1; ell <= nu; ++ell)
       for (int m = 1; m <= M; ++m) {
-        TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c));
+        TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c, m == 1 && ell == 1));
         TRY(reaction_cell(ctx, W, m, ell, dt, sd, c));
       }
     return CISDC_OK;
@@ -880,7 +918,7 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
         CU(cudaStreamWaitEvent(sd, evR(m, ell - 1), 0));
       }
       if (tr) CU(cudaEventRecord(tev(0, m, ell, 0), sd));
-      TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c));
+      TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c, m == 1 && ell == 1));
       if (tr) CU(cudaEventRecord(tev(0, m, ell, 1), sd));
       CU(cudaEventRecord(evD(m, ell), sd));
       CU(cudaStreamWaitEvent(sr, evD(m, ell), 0));

@@ -21,7 +21,14 @@ struct QuadArgs {
   const double* fa[kMaxM + 1];
   const double* fd[kMaxM + 1];
   const double* fr[kMaxM + 1];
-  double* base[kMaxM];
+  double* base[kMaxM];  // base[0] may be null (no reader: fused into rhs0 below)
+  // The first stage right-hand side of the sweep, which reads base row 0 and otherwise only fields
+  // this pass loads anyway, assembled here (k_rhs's expression, same bits): rhs0_kind 1 =
+  // misdcq_sweep m = 0 (base - fc*X), 2 = run_diffusion_cell m = 1 (base + (fc*(X - Y) - fc*Z)).
+  int rhs0_kind;
+  double fc;
+  const double *X, *Y, *Z;
+  double* rhs0;
 };
 
 __global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadArgs q, long long n) {
@@ -39,7 +46,9 @@ __global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadA
 #pragma unroll
     for (int j = 0; j <= kMaxM; ++j)
       if (j <= q.M) acc += q.c[m][j] * s[j];
-    q.base[m][e] = acc;
+    if (m == 0 && q.rhs0_kind == 1) q.rhs0[e] = acc - q.fc * q.X[e];
+    if (m == 0 && q.rhs0_kind == 2) q.rhs0[e] = acc + (q.fc * (q.X[e] - q.Y[e]) - q.fc * q.Z[e]);
+    if (q.base[m]) q.base[m][e] = acc;
   }
 }
 
