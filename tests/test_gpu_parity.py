@@ -364,3 +364,28 @@ def test_rows_2d_ragged(gpu, oracle, n):
     for scheme in (0, 1, 2):
         _, g, c = per_step_compare(oracle, spec, scheme, 1)
         assert np.array_equal(g, c)
+
+
+# ------------------------------------------------------------------ Newton/LU edge values (rtc.cuh deferral)
+
+@pytest.mark.parametrize("scheme", [1, 2])
+def test_newton_exact_zero_concentrations(gpu, oracle, scheme):
+    """Exact zeros (+0.0 and -0.0) in the species the rates multiply by: Jacobian entries and LU
+    multipliers become exact zeros, whose quotients fall outside the branch-free division's range
+    test, so those cells take the exact dense path.  The state must stay bit-identical to the
+    oracle (signed zeros included)."""
+    n = (32, 16, 8)
+    spec = c5_like(n, P.constant_velocity_tables((1.0, -0.5, 0.25), n), seed=5)
+    phi = spec.phi0.reshape(9, n[2], n[1], n[0]).copy()
+    reac, _, _, _ = P._c45_network()
+    partners = sorted({int(b) for a, b in np.asarray(reac).reshape(-1, 2) if b >= 0})
+    for q, s in enumerate(partners[:3]):
+        phi[s, :, 2 + q:10 + q, 3:20] = 0.0
+        phi[s, 1, 12, 5 + q] = -0.0
+    spec.phi0[:] = phi.reshape(-1)
+    for workers in (0, 2) if scheme == 2 else (0,):
+        o = opts(spec, scheme, steps=1, workers=workers)
+        g = api.integrate(spec.problem, spec.phi0, o)
+        c, reps, _ = oracle.integrate(spec.problem, spec.phi0, o)
+        assert np.array_equal(g.final_state.view(np.uint64), c.view(np.uint64))
+        assert g.steps[0].counters.newton_iterations == reps[0].counters.newton_iterations
