@@ -636,6 +636,25 @@ int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters) {
 double QI(const cisdc_tables& t, int m, int j) { return t.QtI[m * t.M + j]; }
 double QE(const cisdc_tables& t, int m, int j) { return t.QtE[m * t.M + j]; }
 
+// The reaction stage of MISDC/MISDCQ adds F_D(phi_AD[m+1]) (integrators.cpp:90,125: a separate
+// eval_diffusion in the reference too).  It is evaluated by the tiled stencil kernels into a
+// scratch field that the Newton kernel then reads pointwise, instead of a (4 ndim + 1)-tap stencil
+// per species inside the FP64-bound Newton kernel: C4 33.3 -> 22.4 ms of Newton per step for 4.2 ms
+// of evaluation.  1-D grids (L2-resident, launch-bound) keep the stencil inside
+// (CISDC_REACT_STENCIL=1: inside everywhere).
+bool react_fd_separate() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_REACT_STENCIL");
+    return !(e && e[0] == '1');
+  }();
+  return v;
+}
+int prepare_fd_ad(cisdc_gpu_ctx* ctx, ReactArgs& a, cudaStream_t s) {
+  if (!react_fd_separate() || ctx->g.ndim < 2) return CISDC_OK;
+  a.fd_ad = ctx->fd_ad[1];
+  return launch_eval_ad(ctx, a.phi_ad, nullptr, ctx->fd_ad[1], s);
+}
+
 // misdcq_sweep (integrators.cpp:103-143)
 int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
   const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
@@ -681,6 +700,7 @@ int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
     a.frp1 = V(ctx, prev, kFr, m + 1);
     a.phi_out = ctx->own[nxt][kPhi][m + 1];
     a.fr_out = ctx->own[nxt][kFr][m + 1];
+    TRY(prepare_fd_ad(ctx, a, s));
     TRY(launch_react(ctx, kModeMisdcq, a, s));
     if (c) ++c->reaction;
     TRY(launch_eval_ad(ctx, ctx->own[nxt][kPhi][m + 1], ctx->own[nxt][kFa][m + 1], ctx->own[nxt][kFd][m + 1], s));
@@ -724,6 +744,7 @@ int sweep_misdc(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
     a.frp1 = V(ctx, prev, kFr, m + 1);
     a.phi_out = ctx->own[nxt][kPhi][m + 1];
     a.fr_out = ctx->own[nxt][kFr][m + 1];
+    TRY(prepare_fd_ad(ctx, a, s));
     TRY(launch_react(ctx, kModeMisdc, a, s));
     if (c) ++c->reaction;
     TRY(launch_eval_ad(ctx, ctx->own[nxt][kPhi][m + 1], ctx->own[nxt][kFa][m + 1], ctx->own[nxt][kFd][m + 1], s));
