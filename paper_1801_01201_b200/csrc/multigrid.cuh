@@ -444,6 +444,116 @@ __global__ void __launch_bounds__(256) k_mg_prolong(double* __restrict__ x, int 
   x[id] = x[id] + v;
 }
 
+// k_mg_restrict on 2-D levels, one coarse cell per thread with its 2 x 2 fine children's taps
+// loaded as 128-bit pairs (columns 2I, 2I+1 are adjacent; fine nx is even): 12 vector loads per
+// coarse cell instead of 4 x 9 scalar ones.  Per child the expression of mg_ax<2>, children summed
+// in k_mg_restrict's order (dy outer, dx inner): same bits.  Grid: (ceil(cx/32), ceil(cy/8), S).
+__global__ void __launch_bounds__(256) k_mg_restrict2_pair(const __grid_constant__ MgCoef C,
+                                                           const double* __restrict__ x,
+                                                           const double* __restrict__ b, int nx, int ny,
+                                                           double* __restrict__ bc, int cx, int cy,
+                                                           const int* __restrict__ active) {
+  const int I = blockIdx.x * 32 + threadIdx.x, J = blockIdx.y * 8 + threadIdx.y, s = blockIdx.z;
+  if (I >= cx || J >= cy || !active[s]) return;
+  const long long nf = (long long)nx * ny;
+  const double* xs = x + (long long)s * nf;
+  const double* bs = b + (long long)s * nf;
+  const int i = 2 * I;
+  auto ld2 = [&](const double* base, int jj, int ii) {
+    return __ldg(reinterpret_cast<const double2*>(base + (unsigned)jj * (unsigned)nx + (unsigned)ii));
+  };
+  const int im2 = wrapi(i - 2, nx), ip2 = wrapi(i + 2, nx);
+  double acc = 0.0;
+#pragma unroll
+  for (int dy = 0; dy < 2; ++dy) {
+    const int j = 2 * J + dy;
+    // row j: x at i-2 .. i+3 ; column taps at rows j-2, j-1, j+1, j+2 for both cells
+    const double2 xl = ld2(xs, j, im2), xc = ld2(xs, j, i), xr = ld2(xs, j, ip2);
+    const double2 ym2 = ld2(xs, wrapi(j - 2, ny), i), ym1 = ld2(xs, wrapi(j - 1, ny), i);
+    const double2 yp1 = ld2(xs, wrapi(j + 1, ny), i), yp2 = ld2(xs, wrapi(j + 2, ny), i);
+    const double2 bv = ld2(bs, j, i);
+    const double g[6] = {xl.x, xl.y, xc.x, xc.y, xr.x, xr.y};  // x taps i-2 .. i+3
+    const double ya[4] = {ym2.x, ym1.x, yp1.x, yp2.x}, yb[4] = {ym2.y, ym1.y, yp1.y, yp2.y};
+#pragma unroll
+    for (int dx = 0; dx < 2; ++dx) {
+      const double* yy = dx == 0 ? ya : yb;
+      const double xcc = g[2 + dx];
+      double lap = 0.0;
+      lap = lap + C.c[s][0] * (-g[dx] + 16.0 * g[dx + 1] - 30.0 * xcc + 16.0 * g[dx + 3] - g[dx + 4]);
+      lap = lap + C.c[s][1] * (-yy[0] + 16.0 * yy[1] - 30.0 * xcc + 16.0 * yy[2] - yy[3]);
+      const double ax = xcc - C.coef * lap;
+      acc = acc + ((dx == 0 ? bv.x : bv.y) - ax);
+    }
+  }
+  bc[(long long)s * cx * cy + (long long)J * cx + I] = acc * 0.25;
+}
+
+// k_mg_prolong for two x-adjacent fine cells per thread (2-D / 3-D; fine nx is even on every level
+// that has a coarser one): fine cells 2I and 2I+1 share the coarse column I, their second columns
+// are I-1 and I+1; 32-bit in-plane offsets, the fine pair read and written as 128-bit words.  Per
+// cell the expression of k_mg_prolong (same bits).  Grid: (ceil(nx/64), ceil(ny/8), nz * S).
+template <int DIM>
+__global__ void __launch_bounds__(256) k_mg_prolong_pair(double* __restrict__ x, int nx, int ny, int nz,
+                                                         const double* __restrict__ ec, int cx, int cy, int cz,
+                                                         const int* __restrict__ active) {
+  const int I = blockIdx.x * 32 + threadIdx.x;  // coarse column = fine pair
+  const int j = blockIdx.y * 8 + threadIdx.y;
+  const unsigned zs = blockIdx.z;
+  const int k = (int)(zs % (unsigned)nz), s = (int)(zs / (unsigned)nz);
+  if (2 * I >= nx || j >= ny || !active[s]) return;
+  const double* e = ec + (long long)s * cx * cy * cz;
+  const int Il = wrapi(I - 1, cx), Ir = wrapi(I + 1, cx);  // second columns of cells 2I and 2I+1
+  int J = j, J2 = j, K = k, K2 = k;
+  if (DIM >= 2) {
+    J = j >> 1;
+    J2 = wrapi((j & 1) ? J + 1 : J - 1, cy);
+  }
+  if (DIM >= 3) {
+    K = k >> 1;
+    K2 = wrapi((k & 1) ? K + 1 : K - 1, cz);
+  }
+  const unsigned cp = (unsigned)cx * (unsigned)cy;
+  auto row = [&](int jj, int kk) { return e + ((unsigned)kk * cp + (unsigned)jj * (unsigned)cx); };
+  double v[2];
+  if (DIM == 2) {
+    const double* r0 = row(J, 0);
+    const double* r1 = row(J2, 0);
+    const double e0 = __ldg(r0 + I), e1 = __ldg(r1 + I);
+    {
+      const double a0 = 0.75 * e0 + 0.25 * __ldg(r0 + Il);
+      const double a1 = 0.75 * e1 + 0.25 * __ldg(r1 + Il);
+      v[0] = 0.75 * a0 + 0.25 * a1;
+    }
+    {
+      const double a0 = 0.75 * e0 + 0.25 * __ldg(r0 + Ir);
+      const double a1 = 0.75 * e1 + 0.25 * __ldg(r1 + Ir);
+      v[1] = 0.75 * a0 + 0.25 * a1;
+    }
+  } else {
+    const double* r00 = row(J, K);
+    const double* r10 = row(J2, K);
+    const double* r01 = row(J, K2);
+    const double* r11 = row(J2, K2);
+    const double e00 = __ldg(r00 + I), e10 = __ldg(r10 + I), e01 = __ldg(r01 + I), e11 = __ldg(r11 + I);
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int I2 = c == 0 ? Il : Ir;
+      const double a00 = 0.75 * e00 + 0.25 * __ldg(r00 + I2);
+      const double a10 = 0.75 * e10 + 0.25 * __ldg(r10 + I2);
+      const double a01 = 0.75 * e01 + 0.25 * __ldg(r01 + I2);
+      const double a11 = 0.75 * e11 + 0.25 * __ldg(r11 + I2);
+      const double b0 = 0.75 * a00 + 0.25 * a10;
+      const double b1 = 0.75 * a01 + 0.25 * a11;
+      v[c] = 0.75 * b0 + 0.25 * b1;
+    }
+  }
+  double2* xp = reinterpret_cast<double2*>(x + (long long)s * ((long long)nx * ny * nz) +
+                                           ((unsigned)k * (unsigned)nx * (unsigned)ny + (unsigned)j * (unsigned)nx +
+                                            (unsigned)(2 * I)));
+  const double2 xv = *xp;
+  *xp = make_double2(xv.x + v[0], xv.y + v[1]);
+}
+
 // The coarse end of a V-cycle in one kernel: levels lc .. L-1 (each at most a few thousand cells)
 // for one species per block, with __syncthreads between the steps instead of a launch per step.
 // Per point the operations of k_mg_smooth / k_mg_restrict / k_mg_prolong, in the order of
@@ -670,6 +780,16 @@ inline bool mg_coarse_enabled() {
   return v;
 }
 
+// prolongation with two fine cells per thread and the 2-D restriction with vector taps
+// (CISDC_MG_PROLONG_PAIR=0: the per-point kernels)
+inline bool mg_pair_prolong() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_MG_PROLONG_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // row-streaming 2-D sweeps (CISDC_MG_ROWS=0: the per-point kernel)
 inline bool mg_rows_enabled() {
   static const bool v = [] {
@@ -846,13 +966,23 @@ struct MgRunner {
     for (int it = 0; it < d.mg_pre; ++it) smooth(l, l > 0 && it == 0);
     MgLevel& Cl = h.lv[l + 1];
     hook->before(kKMgRestrict, s);
-    k_mg_restrict<DIM><<<grid(Cl), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.nx, Lv.ny, Lv.nz, Cl.b, Cl.nx, Cl.ny,
-                                                      Cl.nz, h.d_active);
+    if (DIM == 2 && Lv.nx % 2 == 0 && tile3d_ok(Lv.ncell) && mg_pair_prolong())
+      k_mg_restrict2_pair<<<dim3((unsigned)((Cl.nx + 31) / 32), (unsigned)((Cl.ny + 7) / 8), (unsigned)h.S),
+                            dim3(32, 8), 0, s>>>(C[l], Lv.x, bof(l), Lv.nx, Lv.ny, Cl.b, Cl.nx, Cl.ny, h.d_active);
+    else
+      k_mg_restrict<DIM><<<grid(Cl), block(), 0, s>>>(C[l], Lv.x, bof(l), Lv.nx, Lv.ny, Lv.nz, Cl.b, Cl.nx, Cl.ny,
+                                                        Cl.nz, h.d_active);
     hook->after(kKMgRestrict, s, 0.0);
     charge(kKMgRestrict, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell), false);
     vcycle(l + 1);
     hook->before(kKMgProlong, s);
-    k_mg_prolong<DIM><<<grid(Lv), block(), 0, s>>>(Lv.x, Lv.nx, Lv.ny, Lv.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
+    if (DIM >= 2 && Lv.nx % 2 == 0 && tile3d_ok(Lv.ncell) && mg_pair_prolong())
+      k_mg_prolong_pair<DIM><<<dim3((unsigned)((Lv.nx / 2 + 31) / 32), (unsigned)((Lv.ny + 7) / 8),
+                                    (unsigned)(Lv.nz * h.S)),
+                               dim3(32, 8), 0, s>>>(Lv.x, Lv.nx, Lv.ny, Lv.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz, h.d_active);
+    else
+      k_mg_prolong<DIM><<<grid(Lv), block(), 0, s>>>(Lv.x, Lv.nx, Lv.ny, Lv.nz, Cl.x, Cl.nx, Cl.ny, Cl.nz,
+                                                     h.d_active);
     hook->after(kKMgProlong, s, 0.0);
     charge(kKMgProlong, 8.0 * h.S * (2.0 * Lv.ncell + Cl.ncell), false);
     for (int it = 0; it < d.mg_post; ++it) smooth(l, false);
