@@ -257,6 +257,7 @@ def config_c3(scale: int = 1, seed: int = 3, n_steps: int = 10) -> RunSpec:
                     products=np.array([[1, -1], [2, -1], [0, -1]], dtype=np.int32),
                     rate_constants=np.array([1.0, 1e2, 1e4]), name="c3")
     mg_defaults(p)
+    p.mg_coarse_sweeps = 4  # more coarse-level sweeps do not reduce the V-cycle count (tools/mg_tune.py)
     rng = np.random.default_rng(seed)
     fields = [np.maximum(1.0 / 3.0 + random_fourier_field(rng, (N, N), 32, 0.1, 4), 1e-8) for _ in range(3)]
     return RunSpec(p, to_layout(fields), 1, 4, 6, 1e-3, n_steps, name="c3", schemes=(0, 1, 2))
@@ -282,6 +283,7 @@ def config_c4(scale: int = 1, seed: int = 4, n_steps: int = 2) -> RunSpec:
                     diffusivity=D, reaction_kind=_abi.REACTION_MASS_ACTION, reactants=reac, products=prod,
                     rate_constants=k, newton_tol=1e-12, name="c4")
     mg_defaults(p)
+    p.mg_coarse_sweeps = 2  # two levels here: 2 coarse sweeps already give the V-cycle count of 8
     rng = np.random.default_rng(seed)
     fields = _normalised_fields(rng, (N, N), 9, 32, 4)
     return RunSpec(p, to_layout(fields), 1, 4, 8, 1e-5, n_steps, name="c4", schemes=(0, 1, 2))
