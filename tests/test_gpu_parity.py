@@ -389,3 +389,44 @@ def test_newton_exact_zero_concentrations(gpu, oracle, scheme):
         c, reps, _ = oracle.integrate(spec.problem, spec.phi0, o)
         assert np.array_equal(g.final_state.view(np.uint64), c.view(np.uint64))
         assert g.steps[0].counters.newton_iterations == reps[0].counters.newton_iterations
+
+
+# ------------------------------------------------------------------ multigrid hierarchies (several levels)
+
+def mg_levels(p, coef):
+    """Levels mg_plan uses for this coefficient (the stiffness criterion of multigrid.cuh / the oracle)."""
+    n = list(p.n[: p.ndim])
+    L = 1
+    while all(x % 2 == 0 and x // 2 >= max(p.mg_min_coarse, 4) for x in n):
+        csum = sum(max(p.diffusivity) / (12.0 * (p.h[a] * 2 ** (L - 1)) ** 2) for a in range(p.ndim))
+        emax = 1.0 + coef * 64.0 * csum
+        if (emax - 1.0) / (emax + 1.0) <= 0.1:
+            break
+        n = [x // 2 for x in n]
+        L += 1
+    return L
+
+
+@pytest.mark.parametrize("n", [(128, 96, 1), (64, 32, 1), (64, 32, 48)])
+def test_multigrid_hierarchy_bitwise(gpu, oracle, n):
+    """Stiff diffusion (several multigrid levels: restriction, prolongation, coarse sweeps, the
+    single-block coarse kernel) on 2-D and 3-D grids, C3's reaction chain: bitwise equal to the
+    oracle with equal V-cycle counts, MISDCQ and CISDCQ (serial and concurrent)."""
+    ndim = 3 if n[2] > 1 else 2
+    vel = P.constant_velocity_tables((1.0, -0.5, 0.25), n) if ndim == 3 else P.vortex_tables(n[0], n[1])
+    p = P.ProblemDesc(ndim=ndim, n=n, nspecies=3, h=tuple(1.0 / x for x in n[:ndim]) + (1.0,) * (3 - ndim),
+                      vel=vel, diffusivity=np.array([2.0, 0.5, 0.1]), reaction_kind=_abi.REACTION_MASS_ACTION,
+                      reactants=np.array([[0, -1], [1, -1], [2, -1]], dtype=np.int32),
+                      products=np.array([[1, -1], [2, -1], [0, -1]], dtype=np.int32),
+                      rate_constants=np.array([1.0, 1e2, 1e4]), name="mg-levels")
+    P.mg_defaults(p)
+    p.mg_coarse_sweeps = 4
+    dt = 1e-3
+    assert mg_levels(p, dt * 0.05) >= 3
+    rng = np.random.default_rng(7)
+    shape = n[:ndim]
+    fields = [np.maximum(1.0 / 3.0 + P.random_fourier_field(rng, shape, 16, 0.1, 4), 1e-8) for _ in range(3)]
+    spec = P.RunSpec(p, P.to_layout(fields), 1, 4, 2, dt, 1, name="mg-levels", schemes=(1, 2))
+    for scheme, workers in ((1, 0), (2, 0), (2, 2)):
+        _, g, c = per_step_compare(oracle, spec, scheme, 1, workers=workers)
+        assert np.array_equal(g, c)
