@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadA
   for (int j = 0; j <= kMaxM; ++j)
     if (j <= q.M) s[j] = q.fa[j][e] + q.fd[j][e] + q.fr[j][e];
   const double p0 = q.phi0[e];
+  double acc0 = 0.0;
 #pragma unroll
   for (int m = 0; m < kMaxM; ++m) {
     if (m >= q.M) break;
@@ -46,10 +47,11 @@ __global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadA
 #pragma unroll
     for (int j = 0; j <= kMaxM; ++j)
       if (j <= q.M) acc += q.c[m][j] * s[j];
-    if (m == 0 && q.rhs0_kind == 1) q.rhs0[e] = acc - q.fc * q.X[e];
-    if (m == 0 && q.rhs0_kind == 2) q.rhs0[e] = acc + (q.fc * (q.X[e] - q.Y[e]) - q.fc * q.Z[e]);
+    if (m == 0) acc0 = acc;
     if (q.base[m]) q.base[m][e] = acc;
   }
+  if (q.rhs0_kind == 1) q.rhs0[e] = acc0 - q.fc * q.X[e];
+  else if (q.rhs0_kind == 2) q.rhs0[e] = acc0 + (q.fc * (q.X[e] - q.Y[e]) - q.fc * q.Z[e]);
 }
 
 // One correction term: cE*(A - Ap) + cI*(D - Dp)                 (R == nullptr)
