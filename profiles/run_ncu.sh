@@ -27,6 +27,7 @@ else
   cap mg3 "k_mg3_tiled|k_mg3_pair" 4
   cap eval k_eval_ad3 2
   cap react "^k_react$" 2
-  cap rhs "k_rhs|k_quad|k_mg_update|copy_unswept" 4
+  cap rhs "^k_rhs$" 2
+  cap quad "k_quad|k_mg_update|copy_unswept" 4
 fi
 ls -la gpurun_out

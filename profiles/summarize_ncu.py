@@ -89,7 +89,7 @@ def main():
     traffic = {}
     lines += ["## `--set full` captures", "", "| kernel | " + " | ".join(n for _, n in METRICS) + " | DRAM GB/s |",
               "|---|" + "---:|" * (len(METRICS) + 1)]
-    for part in ("react", "eval", "mg3", "rhs", "all"):
+    for part in ("react", "eval", "mg3", "rhs", "quad", "rhsd", "all"):
         p = os.path.join(d, f"{tag}_{cfg}_{part}_raw.csv")
         if not os.path.exists(p):
             continue
