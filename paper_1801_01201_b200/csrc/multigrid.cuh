@@ -159,8 +159,10 @@ __global__ void k_mg_copy_unswept(const double* __restrict__ b, double* __restri
 }
 
 // per-species stop decision of the oracle's loop: rn <= tol*bn -> done; cap -> failure
+// count == 0: the decision of a check-only pass (no cycle follows it in the same launch sequence;
+// the next cycle's fused check repeats the same decision and counts)
 __global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int* cycles, const double* bmax,
-                            double* rmax, int* flag, DevStatus* st) {
+                            double* rmax, int* flag, DevStatus* st, int count = 1) {
   if (threadIdx.x != 0) return;
   int any = 0;
   for (int s = 0; s < S; ++s) {
@@ -168,6 +170,10 @@ __global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int*
     const double thr = tol * bmax[s];
     if (rmax[s] <= thr) {
       active[s] = 0;
+      continue;
+    }
+    if (!count) {
+      any = 1;
       continue;
     }
     if (cycles[s] >= max_cycles) {
@@ -770,6 +776,15 @@ inline int mg_plan(const MgHierarchy& h, const cisdc_problem_desc& d, double coe
   return L;
 }
 
+// the last check of a predicted batch as a residual-only pass (CISDC_MG_CHECKONLY=0: fused)
+inline bool mg_check_only_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("CISDC_MG_CHECKONLY");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
 // levels of at most this many cells run inside one k_mg_coarse launch (CISDC_MG_COARSE=0: off)
 constexpr long long kMgCoarseCells = 1024;
 inline bool mg_coarse_enabled() {
@@ -801,6 +816,8 @@ inline bool mg_rows_enabled() {
            cudaFuncSetAttribute(k_mg2_rows<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
                cudaSuccess &&
            cudaFuncSetAttribute(k_mg2_rows<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_mg2_rows<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
                cudaSuccess;
   }();
   return v;
@@ -817,6 +834,8 @@ inline bool mg_pair_enabled() {
            cudaFuncSetAttribute(k_mg3_pair<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
                cudaSuccess &&
            cudaFuncSetAttribute(k_mg3_pair<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_mg3_pair<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
                cudaSuccess;
   }();
   return v;
@@ -863,11 +882,38 @@ struct MgRunner {
   dim3 block() const { return stencil_block(DIM); }
 
   // per-species decision of the oracle's loop on the reduced norms (enables the rest of the cycle)
-  void update() {
+  void update(int count = 1) {
     hook->before(kKMgNorm, s);
     k_mg_update<<<1, 32, 0, s>>>(h.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
-                                 h.d_flag, st);
+                                 h.d_flag, st, count);
     hook->after(kKMgNorm, s, 0.0);
+  }
+
+  // The predicted last check of a solve without the sweep fused to it: ||b - A x||_inf of the
+  // level-0 iterate (reads x and b, writes nothing; the fused form also writes a sweep that a
+  // converged species discards), then the decision without counting a cycle.
+  void check_only() {
+    MgLevel& Lv = h.lv[0];
+    const bool pair = DIM == 3 && tile3d_ok(Lv.ncell) && Lv.nx % 2 == 0 && mg_pair_enabled();
+    const bool rows2 = DIM == 2 && Lv.nx % 2 == 0 && Lv.nx >= 64 && tile3d_ok(Lv.ncell) && mg_rows_enabled();
+    hook->before(kKMgSmooth, s);
+    if (rows2) {
+      const int ch = rows_chunk(Lv.ncell, h.S);
+      k_mg2_rows<false, true, false><<<rows_grid(Lv.nx, Lv.ny, h.S, ch), kRowWarps * 32, kRowSmem, s>>>(
+          C[0], Lv.x, b0, nullptr, Lv.nx, Lv.ny, ch, h.d_active, h.d_rmax, nullptr);
+    } else if (pair) {
+      k_mg3_pair<false, true, false><<<tile3d_pair_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), kMgPairSmem, s>>>(
+          C[0], Lv.x, b0, nullptr, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, h.d_rmax, nullptr);
+    } else if (DIM == 3 && tile3d_ok(Lv.ncell)) {
+      k_mg3_tiled<false, true, false><<<tile3d_grid(Lv.nx, Lv.ny, Lv.nz, h.S), dim3(kTX, kTY), 0, s>>>(
+          C[0], Lv.x, b0, nullptr, Lv.nx, Lv.ny, Lv.nz, kZChunk, h.d_active, h.d_rmax, nullptr);
+    } else {
+      const dim3 rb = block();
+      const dim3 rg((Lv.nx + rb.x - 1) / rb.x, (Lv.ny + rb.y - 1) / rb.y, h.S);
+      k_mg_resmax<DIM><<<rg, rb, 0, s>>>(C[0], Lv.x, b0, Lv.nx, Lv.ny, Lv.nz, h.d_active, h.d_rmax, nullptr);
+    }
+    hook->after(kKMgSmooth, s, 0.0);
+    update(0);
   }
 
   void smooth(int l, bool from_zero) {
@@ -1094,7 +1140,8 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   int batch = 1;
   for (const auto& pc : h.predicted)
     if (pc.first == coef) batch = std::max(1, pc.second);
-  int launched = 0;  // V-cycles enqueued
+  int launched = 0;   // V-cycles enqueued
+  int chk_only = -1;  // real cycles enqueued before the check-only pass (-1: none)
   if (fused) {
     // cycle i checks x_{i-1} first: n real cycles need n + 1 enqueued ones.  Cycles after the first
     // replay a captured graph of the cycle (same kernels, same pointers: the sweep counts per level
@@ -1102,8 +1149,16 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     batch += 1;
     const bool use_graph = !hook->timing() && graphs_enabled();
     MgHierarchy::CycleGraph* cg = nullptr;
+    bool first_batch = true;
     for (;;) {
       for (int b = 0; b < batch && launched <= d.mg_max_cycles; ++b, ++launched) {
+        if (first_batch && b == batch - 1 && b >= 1 && mg_check_only_enabled()) {
+          // the predicted convergence check: residual only (a misprediction costs this pass; the
+          // next cycle's fused check repeats the decision)
+          R.check_only();
+          chk_only = b;
+          continue;
+        }
         if (launched >= 1 && use_graph) {
           if (!cg) cg = cycle_graph(h, R, coef, rhs, out, s);
           if (cg) {
@@ -1121,6 +1176,7 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
       if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
       if (!h.h_flag[0] || h.h_flag[1] || launched > d.mg_max_cycles) break;
       batch = 1;
+      first_batch = false;
     }
   } else {
     check();
@@ -1153,9 +1209,16 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     }
     const double per = 1.0 / g.S;
     if (fused) {
-      // the first check sweeps x = b (rhs read once + the partner written), later ones 3 fields
-      const double n8 = 8.0 * (double)n;
-      hook->add_bytes(kKMgSmooth, (2.0 * n8 * g.S + 3.0 * n8 * cycles) * per);
+      // the first check sweeps x = b (rhs read once + the partner written), later ones 3 fields;
+      // the check-only pass (after P = chk_only cycles) reads 2 fields: a species that stopped
+      // there saved one field, one that went on paid it on top
+      double fields = 0.0;
+      for (int v : cyc) {
+        fields += 2.0 + 3.0 * v;
+        if (chk_only >= 1 && v == chk_only) fields -= 1.0;
+        if (chk_only >= 1 && v > chk_only) fields += 2.0;
+      }
+      hook->add_bytes(kKMgSmooth, 8.0 * (double)g.ncell * fields);
     } else {
       hook->add_bytes(kKMgNorm, (8.0 * n * g.S + 16.0 * n * cycles) * per);
     }
