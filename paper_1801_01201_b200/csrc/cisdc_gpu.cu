@@ -587,7 +587,7 @@ int launch_incr(cisdc_gpu_ctx* ctx, const double* a, const double* b, double* ou
   k_incr_partial<<<kIncrBlocks, kIncrThreads, 0, s>>>(a, b, ctx->g.n, ctx->d_partial);
   ctx->tm.after(kKIncr, s, 2.0 * F8(ctx));
   ctx->tm.before(kKIncr, s);
-  k_incr_final<<<1, 512, 0, s>>>(a, b, ctx->g.n, ctx->d_partial, out);
+  k_incr_final<<<1, 1024, 0, s>>>(a, b, ctx->g.n, ctx->d_partial, out);
   ctx->tm.after(kKIncr, s, 0.0);
   CU(cudaGetLastError());
   return CISDC_OK;

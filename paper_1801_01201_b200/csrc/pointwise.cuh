@@ -142,8 +142,9 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
   a.out[e] = r;
 }
 
-constexpr int kIncrBlocks = 296;  // 2 x 148 SMs; fixed so the reduction tree is fixed
+constexpr int kIncrBlocks = 1184;  // 8 x 148 SMs; fixed so the reduction tree is fixed
 constexpr int kIncrThreads = 256;
+static_assert(kIncrBlocks <= 2048, "k_incr_final folds at most two partials per thread");
 
 __global__ void __launch_bounds__(kIncrThreads) k_incr_partial(const double* __restrict__ a,
                                                               const double* __restrict__ b, long long n,
@@ -161,13 +162,16 @@ __global__ void __launch_bounds__(kIncrThreads) k_incr_partial(const double* __r
   if (threadIdx.x == 0) partial[blockIdx.x] = sh[0];
 }
 
-__global__ void k_incr_final(const double* __restrict__ a, const double* __restrict__ b, long long n,
-                             const double* __restrict__ partial, double* __restrict__ out) {
-  __shared__ double sh[512];
+__global__ void __launch_bounds__(1024) k_incr_final(const double* __restrict__ a, const double* __restrict__ b,
+                                                     long long n, const double* __restrict__ partial,
+                                                     double* __restrict__ out) {
+  __shared__ double sh[1024];
   const int t = threadIdx.x;
-  sh[t] = t < kIncrBlocks ? partial[t] : 0.0;
+  double v = t < kIncrBlocks ? partial[t] : 0.0;
+  if (t + 1024 < kIncrBlocks) v = v + partial[t + 1024];
+  sh[t] = v;
   __syncthreads();
-  for (int w = 256; w > 0; w >>= 1) {
+  for (int w = 512; w > 0; w >>= 1) {
     if (t < w) sh[t] = sh[t] + sh[t + w];
     __syncthreads();
   }
