@@ -1194,6 +1194,7 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     }
   }
   // remember how many cycles this coefficient needed (flag[0] == 0 after the last check)
+  bool any_unswept = false;
   {
     std::vector<int> cyc(g.S);
     cudaMemcpy(cyc.data(), h.d_cycles, sizeof(int) * g.S, cudaMemcpyDeviceToHost);
@@ -1206,6 +1207,7 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
       checks += v + 1;
       cycles += v;
       unswept += v == 0;
+      any_unswept = any_unswept || v == 0;
     }
     const double per = 1.0 / g.S;
     if (fused) {
@@ -1242,11 +1244,14 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   L0.x = own_x;
   L0.t = own_t;
   if (!in_out) return CISDC_E_CUDA;  // unreachable with even sweep counts
-  // species that met the tolerance at x = b never had a sweep write `out`
-  const dim3 cg((unsigned)std::min<long long>((g.ncell + 255) / 256, 4096), (unsigned)g.S, 1);
-  hook->before(kKMgNorm, s);
-  k_mg_copy_unswept<<<cg, 256, 0, s>>>(rhs, out, g.ncell, h.d_cycles);
-  hook->after(kKMgNorm, s, 0.0);
+  // species that met the tolerance at x = b never had a sweep write `out` (the host read the cycle
+  // counts above, so the copy is launched only when there is one)
+  if (any_unswept) {
+    const dim3 cg((unsigned)std::min<long long>((g.ncell + 255) / 256, 4096), (unsigned)g.S, 1);
+    hook->before(kKMgNorm, s);
+    k_mg_copy_unswept<<<cg, 256, 0, s>>>(rhs, out, g.ncell, h.d_cycles);
+    hook->after(kKMgNorm, s, 0.0);
+  }
   if (cudaGetLastError() != cudaSuccess) return CISDC_E_CUDA;
   return CISDC_OK;
 }
