@@ -110,7 +110,8 @@ struct Timing final : LaunchHook {
 }  // namespace
 
 struct cisdc_gpu_ctx {
-  cisdc_problem_desc desc{};
+  cisdc_problem_desc desc{};  // borrowed pointers are dropped after create; diffusivity is owned
+  std::vector<double> diffusivity;
   cisdc_tables tb{};
   int M = 0;
   Geom g{};
@@ -138,7 +139,6 @@ struct cisdc_gpu_ctx {
   double* rd_work = nullptr;
   MgHierarchy mg;
   RtcNewton rtc;  // network-specialised Newton kernels (mass action)
-  bool rtc_pad_set[4] = {};
   unsigned* defer_list = nullptr;  // cells the specialised kernel hands to the dense fixup
   int* defer_count = nullptr;
   // status / reductions
@@ -151,16 +151,11 @@ struct cisdc_gpu_ctx {
   unsigned long long newton_seen = 0, mg_seen = 0;
   cudaStream_t s_main = nullptr, s_r = nullptr;
   int num_sms = 148;
-  // optional SM partition for the PMISDC D/R chains (green contexts; CISDC_GREEN_R_SMS = SMs of the
-  // R chain): the two chains then run side by side instead of time-slicing the whole GPU
   // PMISDC schedule trace (cisdc_gpu_set_trace / cisdc_gpu_last_trace)
   bool trace_on = false, trace_pending = false;
   int trace_M = 0, trace_nu = 0, trace_workers = 0;
   std::vector<cudaEvent_t> trace_ev;  // [2 * cell id + 0/1] start/end, last = base
   std::vector<cisdc_cell_trace> trace;
-  CUgreenCtx green[2] = {};
-  CUresult (*green_destroy)(CUgreenCtx) = nullptr;
-  cudaStream_t gs_d = nullptr, gs_r = nullptr;
   std::vector<cudaEvent_t> ev_pool;
   cudaEvent_t ev_base = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
   Timing tm;
@@ -168,6 +163,10 @@ struct cisdc_gpu_ctx {
   std::string err;
   double last_incr = 0.0;
   bool have_incr = false;
+  // failure tags (DevStatus::fail_key): tag t-1 -> (sweep of the running integrate step, stage)
+  std::vector<std::pair<int, int>> tags;
+  int cur_sweep = 0;   // 1-based sweep of the integrate step being enqueued, 0 outside integrate
+  int fail_sweep = 0;  // sweep of the failure the last check_status decoded
 };
 
 namespace {
@@ -215,21 +214,16 @@ void alias_views_to_node0(cisdc_gpu_ctx* c, int set) {
     for (int m = 0; m <= c->M; ++m) c->view[set][f][m] = c->node0[f];
 }
 
+unsigned next_tag(cisdc_gpu_ctx* c, int stage) {
+  c->tags.push_back({c->cur_sweep, stage});
+  return (unsigned)c->tags.size();
+}
+
 int grid_of(long long n, int block) { return static_cast<int>((n + block - 1) / block); }
 
 double F8(const cisdc_gpu_ctx* c) { return 8.0 * (double)c->g.n; }  // bytes of one field
 
 // ---------------------------------------------------------------- kernel launchers
-
-// register budget of the tiled 3-D F_A/F_D kernel: 2 resident blocks (no spills) by default;
-// CISDC_EVAL_MIN_BLOCKS=3 trades a few spills for occupancy (measurement knob)
-int eval_min_blocks() {
-  static const int v = [] {
-    const char* e = std::getenv("CISDC_EVAL_MIN_BLOCKS");
-    return e ? std::atoi(e) : 2;
-  }();
-  return v;
-}
 
 // two cells per thread for F_A/F_D on even-nx 3-D grids (CISDC_EVAL_PAIR=0: one cell per thread)
 bool eval_pair() {
@@ -248,11 +242,7 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
     case 1: k_eval_ad<1><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd); break;
     case 2:
       if (g.nx % 2 == 0 && g.nx >= 64 && tile3d_ok(g.ncell) && eval_pair()) {
-        static bool attr = false;
-        if (!attr) {
-          CU(cudaFuncSetAttribute(k_eval_ad2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
-          attr = true;
-        }
+        CU(func_attr_once(k_eval_ad2_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
         const int ch = rows_chunk(g.ncell, g.S);
         k_eval_ad2_rows<<<rows_grid(g.nx, g.ny, g.S, ch), kRowWarps * 32, kRowSmem, s>>>(ctx->ops, g, phi, fa, fd, ch);
       } else {
@@ -265,12 +255,8 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
         break;
       }
       if (g.nx % 2 == 0 && eval_pair()) {
-        static bool attr = false;
-        if (!attr) {
-          CU(cudaFuncSetAttribute(k_eval_ad3_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
-          CU(cudaFuncSetAttribute(k_eval_ad3_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
-          attr = true;
-        }
+        CU(func_attr_once(k_eval_ad3_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
+        CU(func_attr_once(k_eval_ad3_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
         if (ctx->ops.vconst)
           k_eval_ad3_pair<true><<<tile3d_pair_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), kPairSmem, s>>>(
               ctx->ops, g, phi, fa, fd, kZChunk);
@@ -280,9 +266,6 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
       } else if (ctx->ops.vconst)
         k_eval_ad3_tiled<2, true><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa,
                                                                                                  fd, kZChunk);
-      else if (eval_min_blocks() >= 3)
-        k_eval_ad3_tiled<3, false><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa,
-                                                                                                  fd, kZChunk);
       else
         k_eval_ad3_tiled<2, false><<<tile3d_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), 0, s>>>(ctx->ops, g, phi, fa,
                                                                                                   fd, kZChunk);
@@ -379,7 +362,9 @@ void launch_fixup_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   }
 }
 
-int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t s) {
+int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a_in, cudaStream_t s) {
+  ReactArgs a = a_in;
+  a.tag = next_tag(ctx, CISDC_STAGE_REACTION);
   if (ctx->rtc.ready) {
     Reaction rx = ctx->rx;
     Ops o = ctx->ops;
@@ -389,20 +374,9 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a, cudaStream_t 
     aa.defer_count = ctx->defer_count;
     DevStatus* st = ctx->d_st;
     void* args[5] = {&rx, &o, &g, &aa, &st};
-    // CISDC_REACT_SMEM (bytes, measurement knob): unused dynamic shared memory per block, which caps
-    // the Newton kernel's resident blocks per SM and leaves room for the concurrent D chain's blocks
-    static const int pad = [] {
-      const char* e = std::getenv("CISDC_REACT_SMEM");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (pad > 48 * 1024 && !ctx->rtc_pad_set[mode]) {
-      CU(cudaFuncSetAttribute(reinterpret_cast<const void*>(ctx->rtc.fn[mode]),
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, pad));
-      ctx->rtc_pad_set[mode] = true;
-    }
     ctx->tm.before(kKReact, s);
     CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)), dim3(128),
-                        args, (size_t)pad, s));
+                        args, 0, s));
     ctx->tm.after(kKReact, s, F8(ctx) * react_fields(mode, a));
     // cells whose LU needed a row interchange: dense generic kernel, then reset the list
     ctx->tm.before(kKReact, s);
@@ -511,13 +485,8 @@ int launch_solve1d_e(cisdc_gpu_ctx* ctx, const Solve1dArgs& a, int cl, cudaStrea
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cl > 8) {
-    static bool np = false;  // per instance: clusters above 8 CTAs are opt-in
-    if (!np) {
-      CU(cudaFuncSetAttribute(k_solve1d_periodic<E, T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      np = true;
-    }
-  }
+  if (cl > 8)  // clusters above 8 CTAs are opt-in
+    CU(func_attr_once(k_solve1d_periodic<E, T>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   ctx->tm.before(kKSolve1d, s);
   CU(cudaLaunchKernelEx(&cfg, k_solve1d_periodic<E, T>, a));
   ctx->tm.after(kKSolve1d, s, 2.0 * F8(ctx));
@@ -539,6 +508,7 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
     a.rhs = rhs;
     a.out = out;
     a.work = ctx->rd_work;
+    a.tag = next_tag(ctx, CISDC_STAGE_DIFFUSION);
     ctx->tm.before(kKSolve1d, s);
     k_rd_banded_solve<<<1, 32, 0, s>>>(a, ctx->d_st);
     ctx->tm.after(kKSolve1d, s, 2.0 * F8(ctx));
@@ -546,7 +516,8 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
     return CISDC_OK;
   }
   if (ctx->desc.diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
-    const int rc = mg_solve(ctx->mg, ctx->g, ctx->desc, coef, rhs, out, ctx->d_st, s, &ctx->tm);
+    const int rc = mg_solve(ctx->mg, ctx->g, ctx->desc, coef, rhs, out, ctx->d_st,
+                            next_tag(ctx, CISDC_STAGE_DIFFUSION), s, &ctx->tm);
     if (rc) return set_err(ctx, rc, "multigrid launch failed");
     return CISDC_OK;
   }
@@ -608,26 +579,34 @@ int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters) {
   }
   ctx->newton_seen = h.newton_trips;
   ctx->mg_seen = h.mg_cycles;
-  if (h.code != 0) {
+  ctx->fail_sweep = 0;
+  if (h.fail_key != ~0ull) {
+    const unsigned tag = (unsigned)(h.fail_key >> 35);
+    const int code = (int)((h.fail_key >> 32) & 7);
+    const unsigned long long cell = h.fail_key & 0xffffffffull;
+    const int stage = (tag >= 1 && tag <= ctx->tags.size()) ? ctx->tags[tag - 1].second : CISDC_STAGE_REACTION;
+    ctx->fail_sweep = (tag >= 1 && tag <= ctx->tags.size()) ? ctx->tags[tag - 1].first : 0;
     char buf[256];
-    if (h.stage == CISDC_STAGE_REACTION) {
-      std::snprintf(buf, sizeof(buf), "solve_reaction_implicit: cell %llu: %s", h.first_bad_cell,
-                    h.code == CISDC_E_SOLVE ? "newton: singular jacobian"
-                                            : "newton: no convergence within the iteration cap");
+    if (stage == CISDC_STAGE_REACTION) {
+      std::snprintf(buf, sizeof(buf), "solve_reaction_implicit: cell %llu: %s", cell,
+                    code == CISDC_E_SOLVE ? "newton: singular jacobian"
+                                          : "newton: no convergence within the iteration cap");
     } else if (ctx->ref_rd) {
-      std::snprintf(buf, sizeof(buf), "banded_solve: singular band at column %llu", h.first_bad_cell);
+      std::snprintf(buf, sizeof(buf), "banded_solve: singular band at column %llu", cell);
     } else {
-      std::snprintf(buf, sizeof(buf), "solve_diffusion: multigrid: species %llu: no convergence in %d cycles",
-                    h.first_bad_cell, ctx->desc.mg_max_cycles);
+      std::snprintf(buf, sizeof(buf), "solve_diffusion: multigrid: species %llu: no convergence in %d cycles", cell,
+                    ctx->desc.mg_max_cycles);
     }
     DevStatus z{};  // reset the status word so the context stays usable
-    z.first_bad_cell = ~0ull;
+    z.fail_key = ~0ull;
     z.newton_trips = h.newton_trips;
     z.mg_cycles = h.mg_cycles;
     CU(cudaMemcpy(ctx->d_st, &z, sizeof(z), cudaMemcpyHostToDevice));
-    const int code = (h.stage == CISDC_STAGE_REACTION || ctx->ref_rd) ? CISDC_E_SOLVE : h.code;
-    return set_err(ctx, code, buf);
+    ctx->tags.clear();
+    const int rc = (stage == CISDC_STAGE_REACTION || ctx->ref_rd) ? CISDC_E_SOLVE : code;
+    return set_err(ctx, rc, buf);
   }
+  ctx->tags.clear();
   return CISDC_OK;
 }
 
@@ -899,12 +878,6 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   // cross-stream edges D(m,l) -> R(m,l) and R(m-2,l), R(m-1,l-1), R(m,l-1) -> D(m,l) are events.
   // D cells are totally ordered on their stream (single rhs buffer); R cells write only their slots.
   cudaStream_t sr = ctx->s_r;
-  if (ctx->gs_d) {  // partitioned SMs: both chains on their green streams, joined back into s_main
-    CU(cudaEventRecord(ctx->ev_base, sd));
-    CU(cudaStreamWaitEvent(ctx->gs_d, ctx->ev_base, 0));
-    sd = ctx->gs_d;
-    sr = ctx->gs_r;
-  }
   const size_t ncells = (size_t)M * nu;
   while (ctx->ev_pool.size() < 2 * ncells) {
     cudaEvent_t e;
@@ -951,10 +924,6 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   }
   CU(cudaEventRecord(ctx->ev_join, sr));
   CU(cudaStreamWaitEvent(sd, ctx->ev_join, 0));
-  if (sd != ctx->s_main) {
-    CU(cudaEventRecord(ctx->ev_join, sd));
-    CU(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
-  }
   return CISDC_OK;
 }
 
@@ -985,49 +954,6 @@ int fill_mass_action(const cisdc_problem_desc* d, Reaction& rx, std::string& why
     }
     rx.k[r] = d->rate_constants[r];
   }
-  return 0;
-}
-
-// Two green contexts over disjoint SM sets: `want` SMs (rounded by the driver) for the R chain, the
-// rest for the D chain; one stream in each.  Kernels of the runtime launch on these streams as on
-// any other (the green context is the primary context with a restricted SM set).
-int setup_green(cisdc_gpu_ctx* ctx, int want) {
-  // driver entry points through the runtime (no link-time dependency on libcuda)
-  auto sym = [](const char* name) -> void* {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
-      return nullptr;
-    return fn;
-  };
-  auto pDeviceGet = reinterpret_cast<CUresult (*)(CUdevice*, int)>(sym("cuDeviceGet"));
-  auto pGetRes = reinterpret_cast<CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType)>(sym("cuDeviceGetDevResource"));
-  auto pSplit = reinterpret_cast<CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*,
-                                              unsigned, unsigned)>(sym("cuDevSmResourceSplitByCount"));
-  auto pDesc = reinterpret_cast<CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned)>(sym("cuDevResourceGenerateDesc"));
-  auto pCreate = reinterpret_cast<CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned)>(sym("cuGreenCtxCreate"));
-  auto pStream = reinterpret_cast<CUresult (*)(CUstream*, CUgreenCtx, unsigned, int)>(sym("cuGreenCtxStreamCreate"));
-  ctx->green_destroy = reinterpret_cast<CUresult (*)(CUgreenCtx)>(sym("cuGreenCtxDestroy"));
-  if (!pDeviceGet || !pGetRes || !pSplit || !pDesc || !pCreate || !pStream || !ctx->green_destroy) return 1;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
-  CUdevice cdev;
-  if (pDeviceGet(&cdev, dev) != CUDA_SUCCESS) return 1;
-  CUdevResource all{}, grp[1]{}, rest{};
-  if (pGetRes(cdev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return 1;
-  unsigned ng = 1;
-  if (pSplit(grp, &ng, &all, &rest, 0, (unsigned)want) != CUDA_SUCCESS || ng != 1) return 1;
-  CUdevResourceDesc dr, dd;
-  if (pDesc(&dr, &grp[0], 1) != CUDA_SUCCESS) return 1;
-  if (pDesc(&dd, &rest, 1) != CUDA_SUCCESS) return 1;
-  if (pCreate(&ctx->green[0], dd, cdev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return 1;
-  if (pCreate(&ctx->green[1], dr, cdev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return 1;
-  CUstream sd, sr;
-  if (pStream(&sd, ctx->green[0], CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return 1;
-  if (pStream(&sr, ctx->green[1], CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return 1;
-  ctx->gs_d = sd;
-  ctx->gs_r = sr;
-  std::fprintf(stderr, "cisdc: green contexts: D chain %u SMs, R chain %u SMs\n", rest.sm.smCount, grp[0].sm.smCount);
   return 0;
 }
 
@@ -1098,10 +1024,6 @@ void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
     if (e) cudaEventDestroy(e);
   if (ctx->s_main) cudaStreamDestroy(ctx->s_main);
   if (ctx->s_r) cudaStreamDestroy(ctx->s_r);
-  if (ctx->gs_d) cudaStreamDestroy(ctx->gs_d);
-  if (ctx->gs_r) cudaStreamDestroy(ctx->gs_r);
-  for (CUgreenCtx g : ctx->green)
-    if (g && ctx->green_destroy) ctx->green_destroy(g);
   delete ctx;
 }
 
@@ -1215,6 +1137,19 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
   } else {
     return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown problem kind");
   }
+  // the caller's arrays are borrowed for the duration of create only (include/cisdc_gpu.h): keep
+  // the diffusivities the multigrid plans read at every solve, forget the rest
+  if (d->diffusivity && d->nspecies > 0) {
+    ctx->diffusivity.assign(d->diffusivity, d->diffusivity + d->nspecies);
+    ctx->desc.diffusivity = ctx->diffusivity.data();
+  } else {
+    ctx->diffusivity.assign(std::max(d->nspecies, 1), 0.0);
+    ctx->desc.diffusivity = ctx->diffusivity.data();
+  }
+  for (auto& row : ctx->desc.vel)
+    for (auto& t : row) t = nullptr;
+  ctx->desc.reactants = ctx->desc.products = nullptr;
+  ctx->desc.rate_constants = nullptr;
   g.ncell = (long long)g.nx * g.ny * g.nz;
   g.n = g.ncell * g.S;
   ctx->S = g.S;
@@ -1251,7 +1186,7 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
   ctx->allocs.push_back(v);
   ctx->d_st = static_cast<DevStatus*>(v);
   DevStatus z{};
-  z.first_bad_cell = ~0ull;
+  z.fail_key = ~0ull;
   CU(cudaMemcpy(ctx->d_st, &z, sizeof(z), cudaMemcpyHostToDevice));
   CU(cudaMallocHost(&ctx->h_st, sizeof(DevStatus)));
   TRY(dalloc(ctx, &ctx->d_partial, kIncrBlocks));
@@ -1263,18 +1198,12 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
   // PMISDC: the D chain (s_main: rhs, multigrid, F_A/F_D) is the critical path; the R chain (s_r:
-  // Newton) fills what it leaves, so s_main gets the higher priority (CISDC_STREAM_PRIO=0 disables)
+  // Newton) fills what it leaves, so s_main gets the higher priority
   {
     int lo = 0, hi = 0;
     CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    const char* e = std::getenv("CISDC_STREAM_PRIO");  // 0 none, 1 D chain first, 2 R chain first
-    const int mode = e ? std::atoi(e) : 1;
-    CU(cudaStreamCreateWithPriority(&ctx->s_main, cudaStreamNonBlocking, mode == 1 ? hi : lo));
-    CU(cudaStreamCreateWithPriority(&ctx->s_r, cudaStreamNonBlocking, mode == 2 ? hi : lo));
-    if (const char* g = std::getenv("CISDC_GREEN_R_SMS")) {
-      const int want = std::atoi(g);
-      if (want > 0 && setup_green(ctx, want) != 0) return set_err(ctx, CISDC_E_CUDA, "green context setup failed");
-    }
+    CU(cudaStreamCreateWithPriority(&ctx->s_main, cudaStreamNonBlocking, hi));
+    CU(cudaStreamCreateWithPriority(&ctx->s_r, cudaStreamNonBlocking, lo));
   }
   CU(cudaEventCreateWithFlags(&ctx->ev_base, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
@@ -1445,12 +1374,18 @@ static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_devi
     TRY(do_initialize(ctx));
     cisdc_step_report rep{};
     int done = 0;
+    // the reference's context prefix (integrators.cpp:320-321); the sweep comes from the failure's
+    // tag (the status word is read once per step) or from the sweep that failed to enqueue
     auto fail = [&](int rc) {
-      ctx->err = "integrate: step " + std::to_string(step + 1) + ", sweep " + std::to_string(done + 1) + ": " + ctx->err;
+      const int k = ctx->fail_sweep > 0 ? ctx->fail_sweep : done + 1;
+      ctx->cur_sweep = 0;
+      ctx->err = "integrate: step " + std::to_string(step + 1) + ", sweep " + std::to_string(k) + ": " + ctx->err;
       return rc == CISDC_E_CUDA ? rc : CISDC_E_SOLVE;
     };
+    ctx->fail_sweep = 0;
     if (o->has_stop_tol) {
       for (int k = 1; k <= o->n_sweeps; ++k) {
+        ctx->cur_sweep = k;
         int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters, k - 1);
         if (!rc) {
           CU(cudaMemcpyAsync(ctx->h_incr + (k - 1), ctx->d_incr + (k - 1), sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1462,17 +1397,17 @@ static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_devi
       }
     } else {
       for (int k = 1; k <= o->n_sweeps; ++k) {
+        ctx->cur_sweep = k;
+        done = k - 1;
         const int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters, k - 1);
         if (rc) return fail(rc);
       }
       CU(cudaMemcpyAsync(ctx->h_incr, ctx->d_incr, sizeof(double) * o->n_sweeps, cudaMemcpyDeviceToHost, s));
       const int rc = check_status(ctx, &rep.counters);
-      if (rc) {
-        ctx->err = "integrate: step " + std::to_string(step + 1) + ": " + ctx->err;
-        return rc == CISDC_E_CUDA ? rc : CISDC_E_SOLVE;
-      }
+      if (rc) return fail(rc);
       done = o->n_sweeps;
     }
+    ctx->cur_sweep = 0;
     for (int k = 0; k < done; ++k)
       if (increments) increments[(size_t)step * o->n_sweeps + k] = ctx->h_incr[k];
     ctx->last_incr = ctx->h_incr[done - 1];
@@ -1593,10 +1528,6 @@ int cisdc_gpu_last_trace(cisdc_gpu_ctx* ctx, cisdc_cell_trace* cells, int max_ce
     const int M = ctx->trace_M, nu = ctx->trace_nu, n = 2 * M * nu;
     CU(cudaStreamSynchronize(ctx->s_main));
     CU(cudaStreamSynchronize(ctx->s_r));
-    if (ctx->gs_d) {
-      CU(cudaStreamSynchronize(ctx->gs_d));
-      CU(cudaStreamSynchronize(ctx->gs_r));
-    }
     std::vector<double> t(2 * (size_t)n);
     const cudaEvent_t base = ctx->trace_ev[0];  // start of D(1,1): the sweep's first cell
     for (int id = 0; id < n; ++id)

@@ -8,6 +8,10 @@
 #ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <mutex>
+#include <set>
+#include <tuple>
 #endif
 
 #include "../../include/cisdc_gpu.h"
@@ -18,15 +22,24 @@ constexpr int kMaxM = CISDC_MAX_M;
 constexpr int kMaxS = CISDC_MAX_SPECIES;
 constexpr int kMaxR = CISDC_MAX_REACTIONS;
 
-// Device status word, one per context (written by kernels, read once per sweep).
+// Device status word, one per context (written by kernels, read once per step).
+// fail_key orders failures the way the reference meets them: the host gives every launch that can
+// fail a tag in enqueue (= the reference's serial) order, and a failing kernel records
+//   key = tag << 35 | code << 32 | cell   (atomicMin)
+// so the earliest failing stage wins and, within it, the smallest cell (species for multigrid).
 struct DevStatus {
-  unsigned long long first_bad_cell;  // smallest failing cell index (atomicMin), ~0ull if none
-  int code;                           // CISDC_E_* of the first recorded failure kind
-  int stage;                          // CISDC_STAGE_* of the failure
+  unsigned long long fail_key;        // ~0ull if nothing failed
   unsigned long long newton_trips;    // Newton residual evaluations (atomicAdd)
   unsigned long long mg_cycles;       // multigrid V-cycles
   double incr_partial_unused;
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void record_failure(DevStatus* st, unsigned tag, int code, unsigned long long cell) {
+  atomicMin(&st->fail_key, ((unsigned long long)tag << 35) | ((unsigned long long)(code & 7) << 32) |
+                               (cell & 0xffffffffull));
+}
+#endif
 
 // Grid geometry of one field (species-major, x fastest).
 struct Geom {
@@ -99,6 +112,25 @@ __device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
 
 #ifndef __CUDACC_RTC__
 inline int ceil_div(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// cudaFuncSetAttribute once per (kernel, attribute, value, device): CUDA applies function
+// attributes per device, so a second context on another device sets them again.
+inline cudaError_t func_attr_once(const void* fn, cudaFuncAttribute attr, int value) {
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int, int>> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return cudaErrorInvalidDevice;
+  const auto key = std::make_tuple(fn, (int)attr, value, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count(key)) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, attr, value);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
+}
+template <class F>
+inline cudaError_t func_attr_once(F* fn, cudaFuncAttribute attr, int value) {
+  return func_attr_once(reinterpret_cast<const void*>(fn), attr, value);
+}
 #endif
 
 }  // namespace cisdc_b200

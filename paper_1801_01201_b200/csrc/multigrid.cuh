@@ -46,6 +46,7 @@ struct MgHierarchy {
   double* d_bmax = nullptr;       // [S]
   double* d_rmax = nullptr;       // [S]
   int* d_flag = nullptr;          // [2]: any_active, failed species + 1
+  unsigned* d_tag = nullptr;      // failure tag of the running solve (DevStatus::fail_key)
   int* h_flag = nullptr;          // pinned mirror
   std::vector<std::pair<double, int>> predicted;  // cycles the last solve with this coef needed
   // Captured V-cycles (the cycles after the first of a solve are identical launch sequences for a
@@ -162,7 +163,7 @@ __global__ void k_mg_copy_unswept(const double* __restrict__ b, double* __restri
 // count == 0: the decision of a check-only pass (no cycle follows it in the same launch sequence;
 // the next cycle's fused check repeats the same decision and counts)
 __global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int* cycles, const double* bmax,
-                            double* rmax, int* flag, DevStatus* st, int count = 1) {
+                            double* rmax, int* flag, DevStatus* st, const unsigned* tag, int count = 1) {
   if (threadIdx.x != 0) return;
   int any = 0;
   for (int s = 0; s < S; ++s) {
@@ -179,9 +180,7 @@ __global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int*
     if (cycles[s] >= max_cycles) {
       active[s] = 0;
       if (flag[1] == 0) flag[1] = s + 1;
-      atomicMin(&st->first_bad_cell, (unsigned long long)s);
-      atomicMax(&st->code, (int)CISDC_E_NUMERIC);
-      st->stage = CISDC_STAGE_DIFFUSION;
+      record_failure(st, *tag, CISDC_E_NUMERIC, (unsigned long long)s);
       continue;
     }
     cycles[s] += 1;
@@ -190,6 +189,23 @@ __global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int*
   }
   for (int s = 0; s < S; ++s) rmax[s] = 0.0;
   flag[0] = any;
+}
+
+// per-solve reset of the bookkeeping (one launch instead of memsets and a host copy); the solve's
+// failure tag goes to device memory because captured cycle graphs are replayed across solves
+__global__ void k_mg_begin(int S, int* active, int* cycles, double* bmax, double* rmax, int* flag, unsigned* tag,
+                           unsigned tag_value) {
+  const int s = threadIdx.x;
+  if (s < S) {
+    active[s] = 1;
+    cycles[s] = 0;
+    bmax[s] = 0.0;
+    rmax[s] = 0.0;
+  }
+  if (s == 0) {
+    flag[0] = flag[1] = 0;
+    *tag = tag_value;
+  }
 }
 
 // max of non-negative values, NaN ignored (the oracle's `if (r > m) m = r`)
@@ -730,7 +746,8 @@ inline int mg_init(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d) {
   h.d_bmax = static_cast<double*>(al(sizeof(double) * g.S));
   h.d_rmax = static_cast<double*>(al(sizeof(double) * g.S));
   h.d_flag = static_cast<int*>(al(sizeof(int) * 2));
-  if (!h.d_active || !h.d_cycles || !h.d_bmax || !h.d_rmax || !h.d_flag) return CISDC_E_CUDA;
+  h.d_tag = static_cast<unsigned*>(al(sizeof(unsigned)));
+  if (!h.d_active || !h.d_cycles || !h.d_bmax || !h.d_rmax || !h.d_flag || !h.d_tag) return CISDC_E_CUDA;
   if (cudaMallocHost(&v, sizeof(int) * 2) != cudaSuccess) return CISDC_E_CUDA;
   h.h_flag = static_cast<int*>(v);
   return CISDC_OK;
@@ -807,38 +824,38 @@ inline bool mg_pair_prolong() {
 
 // row-streaming 2-D sweeps (CISDC_MG_ROWS=0: the per-point kernel)
 inline bool mg_rows_enabled() {
-  static const bool v = [] {
+  static const bool env = [] {
     const char* e = std::getenv("CISDC_MG_ROWS");
-    if (e && e[0] == '0') return false;
-    const int sm = (int)kRowSmem;
-    return cudaFuncSetAttribute(k_mg2_rows<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(k_mg2_rows<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(k_mg2_rows<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(k_mg2_rows<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess;
+    return !(e && e[0] == '0');
   }();
-  return v;
+  if (!env) return false;
+  const int sm = (int)kRowSmem;
+  return func_attr_once(k_mg2_rows<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess &&
+         func_attr_once(k_mg2_rows<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess &&
+         func_attr_once(k_mg2_rows<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess &&
+         func_attr_once(k_mg2_rows<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess;
 }
 
 // two cells per thread for the level-0 sweeps on even-nx 3-D grids (CISDC_MG_PAIR=0: one per thread)
 inline bool mg_pair_enabled() {
-  static const bool v = [] {
+  static const bool env = [] {
     const char* e = std::getenv("CISDC_MG_PAIR");
-    if (e && e[0] == '0') return false;
-    const int sm = (int)kMgPairSmem;
-    return cudaFuncSetAttribute(k_mg3_pair<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(k_mg3_pair<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(k_mg3_pair<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess &&
-           cudaFuncSetAttribute(k_mg3_pair<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
-               cudaSuccess;
+    return !(e && e[0] == '0');
   }();
-  return v;
+  if (!env) return false;
+  const int sm = (int)kMgPairSmem;
+  return func_attr_once(k_mg3_pair<true, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess &&
+         func_attr_once(k_mg3_pair<true, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess &&
+         func_attr_once(k_mg3_pair<true, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess &&
+         func_attr_once(k_mg3_pair<false, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) ==
+             cudaSuccess;
 }
 
 // Wraps the engine's hook while a cycle is captured: counts the kernels (the replays are charged
@@ -885,7 +902,7 @@ struct MgRunner {
   void update(int count = 1) {
     hook->before(kKMgNorm, s);
     k_mg_update<<<1, 32, 0, s>>>(h.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
-                                 h.d_flag, st, count);
+                                 h.d_flag, st, h.d_tag, count);
     hook->after(kKMgNorm, s, 0.0);
   }
 
@@ -1088,7 +1105,7 @@ inline MgHierarchy::CycleGraph* cycle_graph(MgHierarchy& h, MgRunner<DIM>& R, do
 // separate residual-norm pass.
 template <int DIM>
 inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
-                        double* out, DevStatus* st, cudaStream_t s, LaunchHook* hook) {
+                        double* out, DevStatus* st, unsigned tag, cudaStream_t s, LaunchHook* hook) {
   const long long n = g.n;
   if (coef == 0.0) {
     if (cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
@@ -1103,12 +1120,9 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
         R.lc = l;
         break;
       }
-  std::vector<int> ones(g.S, 1);
-  cudaMemcpyAsync(h.d_active, ones.data(), sizeof(int) * g.S, cudaMemcpyHostToDevice, s);
-  cudaMemsetAsync(h.d_cycles, 0, sizeof(int) * g.S, s);
-  cudaMemsetAsync(h.d_bmax, 0, sizeof(double) * g.S, s);
-  cudaMemsetAsync(h.d_rmax, 0, sizeof(double) * g.S, s);
-  cudaMemsetAsync(h.d_flag, 0, sizeof(int) * 2, s);
+  hook->before(kKMgNorm, s);
+  k_mg_begin<<<1, 32, 0, s>>>(g.S, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax, h.d_flag, h.d_tag, tag);
+  hook->after(kKMgNorm, s, 0.0);
   // Level 0 iterates directly in `out` (ping-pong with the level-0 workspace; even sweep counts
   // leave the iterate in `out`), and the initial iterate x = b is read straight from the rhs:
   // no copy in, no copy out.
@@ -1157,6 +1171,8 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
           // next cycle's fused check repeats the decision)
           R.check_only();
           chk_only = b;
+          --launched;  // not a V-cycle: the cap counts real cycles only (the (N+1)-th fused check
+                       // must still test x_N and flag the cap)
           continue;
         }
         if (launched >= 1 && use_graph) {
@@ -1257,11 +1273,11 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
 }
 
 inline int mg_solve(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
-                    double* out, DevStatus* st, cudaStream_t s, LaunchHook* hook) {
+                    double* out, DevStatus* st, unsigned tag, cudaStream_t s, LaunchHook* hook) {
   switch (g.ndim) {
-    case 1: return mg_solve_dim<1>(h, g, d, coef, rhs, out, st, s, hook);
-    case 2: return mg_solve_dim<2>(h, g, d, coef, rhs, out, st, s, hook);
-    default: return mg_solve_dim<3>(h, g, d, coef, rhs, out, st, s, hook);
+    case 1: return mg_solve_dim<1>(h, g, d, coef, rhs, out, st, tag, s, hook);
+    case 2: return mg_solve_dim<2>(h, g, d, coef, rhs, out, st, tag, s, hook);
+    default: return mg_solve_dim<3>(h, g, d, coef, rhs, out, st, tag, s, hook);
   }
 }
 

@@ -239,6 +239,7 @@ struct RdSolveArgs {
   const double* rhs;
   double* out;
   double* work;  // n * 10 doubles
+  unsigned tag;  // failure tag (DevStatus::fail_key)
 };
 
 __global__ void k_rd_banded_solve(RdSolveArgs a, DevStatus* st) {
@@ -282,9 +283,7 @@ __global__ void k_rd_banded_solve(RdSolveArgs a, DevStatus* st) {
       }
     }
     if (best == 0.0) {
-      atomicMin(&st->first_bad_cell, (unsigned long long)k);
-      atomicMax(&st->code, (int)CISDC_E_SOLVE);
-      st->stage = CISDC_STAGE_DIFFUSION;
+      record_failure(st, a.tag, CISDC_E_SOLVE, (unsigned long long)k);
       return;
     }
     const int jmax = min(n - 1, k + kl + ku);

@@ -430,3 +430,49 @@ def test_multigrid_hierarchy_bitwise(gpu, oracle, n):
     for scheme, workers in ((1, 0), (2, 0), (2, 2)):
         _, g, c = per_step_compare(oracle, spec, scheme, 1, workers=workers)
         assert np.array_equal(g, c)
+
+
+def _cap_problem(cap):
+    n = (64, 32, 1)
+    p = P.ProblemDesc(ndim=2, n=n, nspecies=3, h=(1 / 64, 1 / 32, 1.0), vel=P.vortex_tables(64, 32),
+                      diffusivity=np.array([2.0, 0.5, 0.1]), reaction_kind=_abi.REACTION_MASS_ACTION,
+                      reactants=np.array([[0, -1], [1, -1], [2, -1]], dtype=np.int32),
+                      products=np.array([[1, -1], [2, -1], [0, -1]], dtype=np.int32),
+                      rate_constants=np.array([1.0, 1e2, 1e4]), name="mg-cap")
+    P.mg_defaults(p)
+    p.mg_coarse_sweeps = 4
+    p.mg_max_cycles = cap
+    return p
+
+
+@pytest.mark.parametrize("cap", [17, 18, 19, 20, 21])
+def test_multigrid_cycle_cap_matches_oracle(gpu, oracle, cap):
+    """mg_max_cycles near the solves' cycle counts (multigrid.cuh cap path): a solve that
+    needs more than the cap must fail exactly where the oracle fails (same step, sweep, species and
+    cycle count in the message), including the sweeps where an earlier solve with the same coefficient
+    predicted a shorter batch (cap 18 / CISDCQ fails in sweep 4, cap 20 / MISDC in sweep 2); a run
+    within the cap is bitwise equal."""
+    rng = np.random.default_rng(1)
+    phi0 = np.abs(1 / 3 + 0.1 * rng.standard_normal(64 * 32 * 3))
+    for scheme in (0, 1, 2):
+        o = api.IntegrateOptions(scheme=scheme, dt=1e-3, n_steps=2, M=4, n_sweeps=4, nu=1)
+        try:
+            c, reps, _ = oracle.integrate(_cap_problem(cap), phi0, o)
+            cerr = None
+        except oracle.OracleError as e:
+            cerr = str(e)
+        try:
+            g = api.integrate(_cap_problem(cap), phi0, o)
+            gerr = None
+        except api.SolveError as e:
+            gerr = str(e)
+        if cerr is None:
+            assert gerr is None, gerr
+            assert np.array_equal(g.final_state, c)
+            assert sum(s.counters.mg_cycles for s in g.steps) == reps[0].counters.mg_cycles
+        else:
+            assert gerr is not None, f"cap {cap} scheme {scheme}: GPU succeeded where the oracle failed: {cerr}"
+            # oracle: "[3] integrate: step s, sweep k: solve_diffusion: multigrid: species i: no convergence
+            # in N cycles (residual ..., target ...)"
+            want = cerr.split("] ", 1)[1].split(" (residual")[0]
+            assert gerr == want, (gerr, want)
