@@ -29,6 +29,25 @@
 
 #include "cisdc_oracle.h"
 
+/* Optional threads for the per-cell loops (env CISDC_ORACLE_THREADS, default 1): every parallel
+   loop below has independent iterations writing disjoint cells, and the reductions are max-norms
+   (order-free) or integer sums, so the results are bit-identical at any thread count.  Used to
+   generate the full-size golden fixtures (tests/golden/make_golden.py --full) in reasonable time;
+   the CPU baselines in bench.py run with 1 thread (the reference's problem stages are serial). */
+static int co_threads(void) {
+  static int t = -1;
+  if (t < 0) {
+    const char* e = getenv("CISDC_ORACLE_THREADS");
+    t = e ? atoi(e) : 1;
+    if (t < 1) t = 1;
+  }
+  return t;
+}
+#define CO_PRAGMA(x) _Pragma(#x)
+#define CO_PAR_ROWS(n) \
+  CO_PRAGMA(omp parallel for schedule(static) collapse(2) if (co_threads() > 1 && (n) > 16384) num_threads(co_threads()))
+#define CO_PAR(n) CO_PRAGMA(omp parallel for schedule(static) if (co_threads() > 1 && (n) > 16384) num_threads(co_threads()))
+
 #define MAXS CISDC_MAX_SPECIES
 #define MAXR CISDC_MAX_REACTIONS
 #define MAXL 16
@@ -247,6 +266,7 @@ static void adr_advection(const co_problem* p, const double* phi, double* out) {
   for (int s = 0; s < p->S; ++s) {
     const double* f = phi + (size_t)s * p->ncell;
     double* o = out + (size_t)s * p->ncell;
+    CO_PAR_ROWS(p->ncell)
     for (int k = 0; k < p->nz; ++k)
       for (int j = 0; j < p->ny; ++j)
         for (int i = 0; i < p->nx; ++i) {
@@ -275,6 +295,7 @@ static void adr_diffusion(const co_problem* p, const double* phi, double* out) {
   for (int s = 0; s < p->S; ++s) {
     const double* f = phi + (size_t)s * p->ncell;
     double* o = out + (size_t)s * p->ncell;
+    CO_PAR_ROWS(p->ncell)
     for (int k = 0; k < p->nz; ++k)
       for (int j = 0; j < p->ny; ++j)
         for (int i = 0; i < p->nx; ++i) {
@@ -334,8 +355,9 @@ static void adr_reaction(const co_problem* p, const double* phi, double* out) {
       for (size_t i = 0; i < nc; ++i) out[i] = bistable_R(p->d.lambda, p->d.theta, phi[i]);
       break;
     case CISDC_REACTION_MASS_ACTION: {
-      double x[MAXS] = {0}, R[MAXS];
+      CO_PAR(nc)
       for (size_t c = 0; c < nc; ++c) {
+        double x[MAXS] = {0}, R[MAXS];
         for (int s = 0; s < p->S; ++s) x[s] = phi[(size_t)s * nc + c];
         ma_rates(p, x, R);
         for (int s = 0; s < p->S; ++s) out[(size_t)s * nc + c] = R[s];
@@ -449,24 +471,37 @@ static int adr_solve_reaction(co_problem* p, double coef, const double* rhs, dou
     memcpy(out, rhs, sizeof(double) * p->dim);
     return CISDC_OK;
   }
+  /* cells are independent: the first failing cell (the one the reference's serial loop stops at)
+     is the smallest failing index */
+  size_t bad = (size_t)-1;
+  int bad_r = CISDC_OK;
+#pragma omp parallel for schedule(dynamic, 4096) reduction(+ : trips) if (co_threads() > 1 && nc > 16384) \
+    num_threads(co_threads())
   for (size_t cell = 0; cell < nc; ++cell) {
     int r;
+    long long t = 0;
     if (p->d.reaction_kind == CISDC_REACTION_MASS_ACTION) {
       double b[MAXS], x[MAXS];
       for (int s = 0; s < p->S; ++s) b[s] = rhs[(size_t)s * nc + cell];
-      r = newton_vector_cell(p, coef, b, x, &trips);
+      r = newton_vector_cell(p, coef, b, x, &t);
       for (int s = 0; s < p->S; ++s) out[(size_t)s * nc + cell] = x[s];
     } else {
-      r = newton_scalar_cell(p, coef, rhs[cell], &out[cell], &trips);
+      r = newton_scalar_cell(p, coef, rhs[cell], &out[cell], &t);
     }
+    trips += t;
     if (r != CISDC_OK) {
-      rc = -r;
-      snprintf(p->err, sizeof(p->err), "solve_reaction_implicit: cell %zu: %s", cell,
-               rc == CISDC_E_SOLVE ? "newton: singular jacobian"
-                                   : "newton: no convergence within the iteration cap");
-      rc = CISDC_E_SOLVE; /* reaction_diffusion.cpp:178-180 wraps every failure as SolveError */
-      break;
+#pragma omp critical(co_newton_fail)
+      if (cell < bad) {
+        bad = cell;
+        bad_r = r;
+      }
     }
+  }
+  if (bad != (size_t)-1) {
+    rc = -bad_r;
+    snprintf(p->err, sizeof(p->err), "solve_reaction_implicit: cell %zu: %s", bad,
+             rc == CISDC_E_SOLVE ? "newton: singular jacobian" : "newton: no convergence within the iteration cap");
+    rc = CISDC_E_SOLVE; /* reaction_diffusion.cpp:178-180 wraps every failure as SolveError */
   }
   if (c) c->newton_iterations += trips;
   return rc;
@@ -770,6 +805,7 @@ static void mg_smooth(const mg_level_op* L, const double* b, double* x, double* 
     for (size_t i = 0; i < n; ++i) x[i] = L->wD * b[i];
     return;
   }
+  CO_PAR_ROWS(n)
   for (int k = 0; k < L->nz; ++k)
     for (int j = 0; j < L->ny; ++j)
       for (int i = 0; i < L->nx; ++i) {
@@ -782,19 +818,30 @@ static void mg_smooth(const mg_level_op* L, const double* b, double* x, double* 
 
 static double mg_resnorm(const mg_level_op* L, const double* b, const double* x) {
   double m = 0.0;
+  const size_t n = (size_t)L->nx * L->ny * L->nz;
+  /* `if (r > m) m = r` keeps the largest non-NaN residual in any order: per-thread maxima combined
+     with the same rule give the serial result */
+#pragma omp parallel if (co_threads() > 1 && n > 16384) num_threads(co_threads())
+  {
+    double mt = 0.0;
+#pragma omp for schedule(static) collapse(2) nowait
   for (int k = 0; k < L->nz; ++k)
     for (int j = 0; j < L->ny; ++j)
       for (int i = 0; i < L->nx; ++i) {
         const size_t id = ((size_t)k * L->ny + j) * L->nx + i;
         const double r = fabs(b[id] - mg_ax(L, x, i, j, k));
-        if (r > m) m = r;
+        if (r > mt) mt = r;
       }
+#pragma omp critical(co_resnorm)
+    if (mt > m) m = mt;
+  }
   return m;
 }
 
 static void mg_restrict(const mg_level_op* F, const double* b, const double* x, const mg_level_op* C, double* bc) {
   const double scale = F->ndim == 1 ? 0.5 : (F->ndim == 2 ? 0.25 : 0.125);
   const int ez = F->ndim >= 3 ? 2 : 1, ey = F->ndim >= 2 ? 2 : 1;
+  CO_PAR_ROWS((size_t)F->nx * F->ny * F->nz)
   for (int K = 0; K < C->nz; ++K)
     for (int J = 0; J < C->ny; ++J)
       for (int I = 0; I < C->nx; ++I) {
@@ -811,6 +858,7 @@ static void mg_restrict(const mg_level_op* F, const double* b, const double* x, 
 }
 
 static void mg_prolong_add(const mg_level_op* F, double* x, const mg_level_op* C, const double* e) {
+  CO_PAR_ROWS((size_t)F->nx * F->ny * F->nz)
   for (int k = 0; k < F->nz; ++k)
     for (int j = 0; j < F->ny; ++j)
       for (int i = 0; i < F->nx; ++i) {

@@ -20,6 +20,7 @@ from paper_1801_01201_b200 import _abi
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_LIB = os.path.join(HERE, "_build", "libcisdc_oracle.so")
 REF_LIB = os.path.join(HERE, "_ref", "libcisdc_ref.so")
+ENGINE_LIB = os.path.join(HERE, "_ref", "libcisdc_engine_check.so")
 REF_SRC = "/root/reference/proj/core"
 
 _dp = C.POINTER(C.c_double)
@@ -41,6 +42,36 @@ def build_ref() -> str | None:
     if os.path.isdir(REF_SRC):
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True, capture_output=True)
     return REF_LIB if os.path.exists(REF_LIB) else None
+
+
+def build_engine_check() -> str | None:
+    """integration/engine_check.cpp against the reference headers + oracle/_ref + libcisdc_gpu.so."""
+    if os.path.isdir(REF_SRC):
+        r = subprocess.run(["make", "-s", "-C", HERE, "engine"], capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("engine_check build failed:\n" + r.stdout + r.stderr)
+    return ENGINE_LIB if os.path.exists(ENGINE_LIB) else None
+
+
+_engine = None
+
+
+def engine_lib() -> C.CDLL | None:
+    """The compiled reference-side consumer of the GPU engine (None when it was never built)."""
+    global _engine
+    if _engine is None:
+        if not os.path.exists(ENGINE_LIB) and build_engine_check() is None:
+            return None
+        lib = C.CDLL(ENGINE_LIB)
+        ll = C.POINTER(C.c_longlong)
+        lib.engine_vs_reference.argtypes = [C.POINTER(_abi.ProblemDescC), _dp, C.c_size_t,
+                                            C.POINTER(_abi.IntegrateOptionsC), C.c_int, _dp, _dp, ll, ll, _dp, _dp,
+                                            ll, _cp, C.c_size_t]
+        lib.engine_exceptions.argtypes = [C.POINTER(_abi.ProblemDescC), _dp, C.c_size_t,
+                                          C.POINTER(_abi.IntegrateOptionsC), C.c_int, C.POINTER(C.c_int), _cp,
+                                          C.POINTER(C.c_int), _cp, C.c_size_t]
+        _engine = lib
+    return _engine
 
 
 def oracle_lib() -> C.CDLL:

@@ -414,16 +414,21 @@ int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
   } else {
     in.push_back(a.base);
     for (int t = 0; t < a.nt; ++t) {
-      if (a.t[t].diff) in.insert(in.end(), {a.t[t].A, a.t[t].D});
-      else in.insert(in.end(), {a.t[t].A, a.t[t].Ap, a.t[t].D, a.t[t].Dp, a.t[t].R, a.t[t].Rp});
+      const RhsTerm& T = a.t[t];
+      if (!T.skipA && T.diff && T.dA) in.push_back(T.dA);
+      else if (!T.skipA) in.insert(in.end(), {T.A, T.Ap});
+      if (T.diff) in.push_back(T.D);
+      else in.insert(in.end(), {T.D, T.Dp, T.R, T.Rp});
     }
   }
   in.insert(in.end(), {a.X, a.Y, a.Z});
   double outs = 1 + (a.out2 != nullptr) + (a.base_out != nullptr);
-  for (int t = 0; t < a.nt; ++t) outs += a.t[t].outA ? 2 : 0;
+  for (int t = 0; t < a.nt; ++t) outs += (a.t[t].outA != nullptr) + (a.t[t].outDR != nullptr);
   const double fields = distinct_fields(in) + outs;
+  RhsArgs aw = a;
+  aw.wild = ctx->ops.wild;
   ctx->tm.before(kKRhs, s);
-  k_rhs<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(a, ctx->g.n);
+  k_rhs<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(aw, ctx->g.n);
   ctx->tm.after(kKRhs, s, F8(ctx) * fields);
   CU(cudaGetLastError());
   return CISDC_OK;
@@ -656,6 +661,7 @@ int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
       RhsTerm& t = r.t[j - 1];
       t.cE = dt * QE(ctx->tb, m, j - 1);
       t.cI = dt * QI(ctx->tb, m, j - 1);
+      t.skipA = t.cE == 0.0;
       t.A = V(ctx, nxt, kFa, j);
       t.Ap = V(ctx, prev, kFa, j);
       t.D = V(ctx, nxt, kFd, j);
@@ -778,20 +784,23 @@ RhsArgs diffusion_rhs(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double
     RhsTerm& t = r.t[nt++];
     t.cE = dt * QE(ctx->tb, row, j - 1);
     t.cI = dt * QI(ctx->tb, row, j - 1);
+    t.skipA = t.cE == 0.0;  // literal convention: every j <= m - 2 (k_rhs reads A, Ap only where needed)
+    t.A = W.get(2, j, ell);
+    t.Ap = V(ctx, prev, kFa, j);
+    // the dA cache is needed only when some row reads cE * dA (cumulative convention)
+    const bool cache_a = !t.skipA;
     if (cache && j < m - 2) {
       t.diff = 1;
-      t.A = ctx->diff_bufs[2 * (j - 1)];
+      t.dA = cache_a ? ctx->diff_bufs[2 * (j - 1)] : nullptr;
       t.D = ctx->diff_bufs[2 * (j - 1) + 1];
       continue;
     }
-    t.A = W.get(2, j, ell);
-    t.Ap = V(ctx, prev, kFa, j);
     t.D = W.get(3, j, ell);
     t.Dp = V(ctx, prev, kFd, j);
     t.R = W.get(4, j, ell);
     t.Rp = V(ctx, prev, kFr, j);
     if (cache && j <= ctx->M - 3) {
-      t.outA = ctx->diff_bufs[2 * (j - 1)];
+      t.outA = cache_a ? ctx->diff_bufs[2 * (j - 1)] : nullptr;
       t.outDR = ctx->diff_bufs[2 * (j - 1) + 1];
     }
   }
@@ -959,6 +968,7 @@ int fill_mass_action(const cisdc_problem_desc* d, Reaction& rx, std::string& why
 
 int do_initialize(cisdc_gpu_ctx* ctx) {
   cudaStream_t s = ctx->s_main;
+  CU(cudaMemsetAsync(ctx->ops.wild, 0, sizeof(int), s));  // every F_A is evaluated afresh from here
   TRY(launch_eval_ad(ctx, ctx->node0[kPhi], ctx->node0[kFa], ctx->node0[kFd], s));
   TRY(launch_eval_r(ctx, ctx->node0[kPhi], ctx->node0[kFr], s));
   ctx->cur = 0;
@@ -1181,6 +1191,13 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     const int rc = mg_init(ctx->mg, g, *d);
     if (rc) return set_err(ctx, rc, "multigrid: hierarchy setup failed (" + std::to_string(rc) + ")");
   }
+  {
+    void* w = nullptr;
+    CU(cudaMalloc(&w, sizeof(int)));
+    ctx->allocs.push_back(w);
+    ctx->ops.wild = static_cast<int*>(w);
+    CU(cudaMemset(ctx->ops.wild, 0, sizeof(int)));
+  }
   void* v = nullptr;
   CU(cudaMalloc(&v, sizeof(DevStatus)));
   ctx->allocs.push_back(v);
@@ -1252,6 +1269,7 @@ int cisdc_gpu_set_nodes(cisdc_gpu_ctx* ctx, const double* values, size_t n) {
   ctx->cur = 0;
   reset_views(ctx, 0);
   reset_views(ctx, 1);
+  CU(cudaMemsetAsync(ctx->ops.wild, 0, sizeof(int), s));
   for (int m = 0; m <= ctx->M; ++m) {
     double* phi = m == 0 ? ctx->node0[kPhi] : ctx->own[0][kPhi][m];
     double* fa = m == 0 ? ctx->node0[kFa] : ctx->own[0][kFa][m];

@@ -63,7 +63,19 @@ struct Ops {
   // reference Dirichlet problem (CISDC_PROBLEM_REFERENCE_RD)
   int ref_rd;
   double rd_cadv, rd_cdiff, rd_w[2][5];
+  // set (sticky until the next initialize) when an F_A evaluation stores a value with |v| >= 2^1022,
+  // an Inf or a NaN: k_rhs then evaluates cE*(A - Ap) even where cE == 0 (see k_rhs)
+  int* wild;
 };
+
+// |v| >= 2^1022, Inf or NaN (exponent field >= 2045): a difference of two values below this bound
+// is finite, so 0.0 * (A - Ap) is a signed zero
+__device__ __forceinline__ unsigned wild_bits(double v) {
+  return (unsigned)(((unsigned)__double2hiint(v) & 0x7ff00000u) >= (2045u << 20));
+}
+__device__ __forceinline__ void flag_wild(int* flag, unsigned w) {
+  if (w && flag) atomicOr(flag, 1);
+}
 
 // Kernel classes for the live per-class CUDA-event timing (cisdc_gpu_kernel_times).
 enum KernelClass {

@@ -57,12 +57,22 @@ __global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadA
 // One correction term: cE*(A - Ap) + cI*(D - Dp)                 (R == nullptr)
 //                   or cE*(A - Ap) + cI*(D - Dp + R - Rp)
 // CISDCQ difference cache: a term whose differences dA = A - Ap and dDR = ((D - Dp) + R) - Rp were
-// stored by an earlier launch reads just those two fields (diff != 0: A = dA, D = dDR); a term
-// read in full can store them (outA/outDR) for the later nodes.  Same operations, same bits.
+// stored by an earlier launch reads just those (diff != 0: D = dDR, dA = the cached dA or null); a
+// term read in full can store them (outA/outDR) for the later nodes.  Same operations, same bits.
+//
+// Exact zeros (skipA): in the literal Euler convention the configs use, QtE(m, j) is non-zero only
+// on the subdiagonal (reference quadrature.cpp:137-139), so most terms have cE == 0.0.  For finite
+// A - Ap, cE * (A - Ap) is then a signed zero, and t = (+-0) + tI equals tI bit for bit whenever
+// tI = cI * (...) != 0.  Such a term skips the A / Ap reads (and the dA cache): A and Ap are read
+// only at the elements where tI is itself a zero (the sign of the sum then depends on both), and
+// everywhere once an F_A evaluation flagged a value >= 2^1022, an Inf or a NaN (Ops::wild), where
+// the difference could overflow or carry a NaN.  A and Ap are always the original fields.
 struct RhsTerm {
   double cE, cI;
   const double *A, *Ap, *D, *Dp, *R, *Rp;
+  const double* dA;  // cached A - Ap (diff terms whose cE != 0)
   int diff;
+  int skipA;
   double *outA, *outDR;
 };
 
@@ -87,7 +97,15 @@ struct RhsArgs {
   const double* phim;
   const double *sfa[kMaxM + 1], *sfd[kMaxM + 1], *sfr[kMaxM + 1];
   double* base_out;
+  const int* wild;  // Ops::wild of the context
 };
+
+// cE * (A - Ap) + tI with the skipA shortcut above
+__device__ __forceinline__ double rhs_term_a(const RhsTerm& T, long long e, double tI, bool skip) {
+  if (skip && tI != 0.0) return tI;
+  const double dA = (T.diff && T.dA) ? T.dA[e] : T.A[e] - T.Ap[e];
+  return T.cE * dA + tI;
+}
 
 __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, long long n) {
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -101,6 +119,7 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
     a.out[e] = base + a.fc * (a.X[e] - a.Y[e] - a.Z[e]);
     return;
   }
+  const bool tame = a.wild == nullptr || *a.wild == 0;
   const double base = a.base[e];
   if (a.kind == kRhsMisdcq) {
     double rd = base, rr = base;
@@ -108,10 +127,22 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
     for (int t = 0; t < kMaxM; ++t) {
       if (t >= a.nt) break;
       const RhsTerm& T = a.t[t];
-      const double dA = T.A[e] - T.Ap[e];
+      const bool skip = T.skipA && tame;
       const double dD = T.D[e] - T.Dp[e];
-      rd += T.cE * dA + T.cI * dD;
-      if (a.out2) rr += T.cE * dA + T.cI * (dD + T.R[e] - T.Rp[e]);
+      const double tI = T.cI * dD;
+      if (!a.out2) {
+        rd += rhs_term_a(T, e, tI, skip);
+        continue;
+      }
+      const double tI2 = T.cI * (dD + T.R[e] - T.Rp[e]);
+      if (skip && tI != 0.0 && tI2 != 0.0) {
+        rd += tI;
+        rr += tI2;
+      } else {
+        const double cA = T.cE * (T.A[e] - T.Ap[e]);
+        rd += cA + tI;
+        rr += cA + tI2;
+      }
     }
     rd -= a.fc * a.X[e];
     a.out[e] = rd;
@@ -124,19 +155,21 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
   for (int t = 0; t < kMaxM; ++t) {
     if (t >= a.nt) break;
     const RhsTerm& T = a.t[t];
-    double dA, dDR;
+    double dDR;
     if (T.diff) {
-      dA = T.A[e];
       dDR = T.D[e];
     } else {
-      dA = T.A[e] - T.Ap[e];
       dDR = T.D[e] - T.Dp[e] + T.R[e] - T.Rp[e];
-      if (T.outA) {
-        T.outA[e] = dA;
-        T.outDR[e] = dDR;
-      }
+      if (T.outDR) T.outDR[e] = dDR;
     }
-    r += T.cE * dA + T.cI * dDR;
+    const double tI = T.cI * dDR;
+    if (T.skipA && tame) {
+      r += rhs_term_a(T, e, tI, true);
+    } else {
+      const double dA = (T.diff && T.dA) ? T.dA[e] : T.A[e] - T.Ap[e];
+      if (!T.diff && T.outA) T.outA[e] = dA;
+      r += T.cE * dA + tI;
+    }
   }
   r += a.fc * (a.X[e] - a.Y[e]) - a.fc * a.Z[e];
   a.out[e] = r;

@@ -118,11 +118,19 @@ __global__ void __launch_bounds__(256) k_eval_ad(Ops o, Geom g, const double* __
   const long long e = (long long)s * g.ncell + p.cell;
   const double* f = phi + (long long)s * g.ncell;
   if (o.ref_rd) {
-    if (fa) fa[e] = rd_adv(o, f, g.nx, i);
+    if (fa) {
+      const double v = rd_adv(o, f, g.nx, i);
+      fa[e] = v;
+      flag_wild(o.wild, wild_bits(v));
+    }
     if (fd) fd[e] = rd_diff(o, f, g.nx, i);
     return;
   }
-  if (fa) fa[e] = adv_periodic<DIM>(o, g, f, i, j, k);
+  if (fa) {
+    const double v = adv_periodic<DIM>(o, g, f, i, j, k);
+    fa[e] = v;
+    flag_wild(o.wild, wild_bits(v));
+  }
   if (fd) fd[e] = diff_periodic<DIM>(o, g, f, s, i, j, k);
 }
 

@@ -169,7 +169,10 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_eval_ad2_rows(Ops o, Geom
               acc[c] = acc[c] + (fr - fl) * ca1;
             }
           }
-          if (ok) __stcg(reinterpret_cast<double2*>(fas + cell), make_double2(-acc[0], -acc[1]));
+          if (ok) {
+            __stcg(reinterpret_cast<double2*>(fas + cell), make_double2(-acc[0], -acc[1]));
+            flag_wild(o.wild, wild_bits(acc[0]) | wild_bits(acc[1]));
+          }
         }
         if (fds) {
           double lap[2];

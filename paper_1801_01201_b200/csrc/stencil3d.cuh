@@ -253,7 +253,10 @@ __global__ void __launch_bounds__(kTX* kTY, MINB) k_eval_ad3_tiled(Ops o, Geom g
             if (a == 2) fz_carry = fr;
             acc = acc + (fr - fl) * ca[a];
           }
-          if (ok) __stcg(fas + cell, -acc);
+          if (ok) {
+            __stcg(fas + cell, -acc);
+            flag_wild(o.wild, wild_bits(acc));
+          }
         }
         if (fds) {
           double lap = 0.0;
@@ -500,6 +503,7 @@ __global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_pair(Ops 
           }
           if (ok) {
             __stcg(reinterpret_cast<double2*>(fas + cell), make_double2(-acc[0], -acc[1]));
+            flag_wild(o.wild, wild_bits(acc[0]) | wild_bits(acc[1]));
           }
         }
         if (fds) {

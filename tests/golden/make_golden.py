@@ -9,9 +9,24 @@ against them without needing /root/reference.
                   dt = 0.05, M = 4, 3 steps x 4 sweeps): misdc, misdcq, cisdcq nu = 1/3, both conventions
   periodic.npz    the reference integrators driving the periodic ADR problem class (configs 1-5 at
                   reduced size): final state, increments, solve / Newton / multigrid counts
+  full_<cfg>.json (--full [c3 c4 c5]) the same at the BASELINE configs' FULL sizes, one time step:
+                  C3 1024^2 x 3 (misdc, misdcq, cisdcq), C4 2048^2 x 9 (misdc, misdcq, cisdcq),
+                  C5 256^3 x 9 (cisdcq nu = 1 through execute_pipelined, the bench workload).  The
+                  states are too large to commit, so the fixture holds the sha256 of the initial and
+                  final state bytes, per-step counts (sweeps, D/R solves, Newton trips, multigrid
+                  cycles), the increments and a few norms (hex floats), plus the run's host, threads
+                  and wall time.  C5 needs ~100 GB of host RAM (the reference's SweepState layout):
+                  generate it on the GPU box's host (196 GB), e.g.
+                    CISDC_ORACLE_THREADS=16 python tests/golden/make_golden.py --full c5
+                  (the oracle problem class's per-cell loops are threaded; results are bit-identical
+                  at any thread count, see oracle/co_problems.c).
 """
+import hashlib
+import json
 import os
+import platform
 import sys
+import time
 
 import numpy as np
 
@@ -39,7 +54,65 @@ def periodic_runs(name):
     return spec, schemes
 
 
+FULL = {
+    "c3": (lambda: P.config_c3(n_steps=1), (0, 1, 2)),
+    "c4": (lambda: P.config_c4(n_steps=1), (0, 1, 2)),
+    "c5": (lambda: P.config_c5(n_steps=1), (2,)),
+}
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def norms(a: np.ndarray) -> dict:
+    return {"max": float(a.max()).hex(), "min": float(a.min()).hex(), "absmax": float(np.abs(a).max()).hex(),
+            "sum": float(np.sum(a, dtype=np.float64)).hex()}
+
+
+def full(names):
+    """Full-size fixtures through the unmodified reference (oracle/_ref)."""
+    if O.ref_lib() is None:
+        raise SystemExit("oracle/_ref not available (it travels prebuilt; build it where /root/reference exists)")
+    for name in names:
+        make, schemes = FULL[name]
+        t0 = time.time()
+        spec = make()
+        gen_s = time.time() - t0
+        out = {"config": name, "grid": list(spec.problem.n[: spec.problem.ndim]), "species": spec.problem.nspecies,
+               "M": spec.M, "n_sweeps": spec.n_sweeps, "dt": spec.dt, "n_steps": 1, "nu": 1,
+               "phi0_sha256": sha(spec.phi0), "generated_by": "oracle/_ref (unmodified cisdc::integrate / "
+               "cisdc::execute_pipelined) driving the oracle problem class",
+               "host": {"node": platform.node(), "nproc": os.cpu_count(),
+                        "oracle_threads": int(os.environ.get("CISDC_ORACLE_THREADS", "1"))},
+               "phi0_seconds": gen_s, "runs": {}}
+        for s in schemes:
+            workers = min(os.cpu_count() or 1, 6) if s == 2 else 0
+            o = api.IntegrateOptions(scheme=s, dt=spec.dt, n_steps=1, M=spec.M, n_sweeps=spec.n_sweeps, nu=1,
+                                     workers=workers)
+            t0 = time.time()
+            f, reps, incs = O.ref_integrate(spec.problem, spec.phi0, o)
+            wall = time.time() - t0
+            r = reps[0]
+            out["runs"][str(s)] = {
+                "scheme": ["misdc", "misdcq", "cisdcq"][s], "workers": workers, "seconds": wall,
+                "final_sha256": sha(f), "final_norms": norms(f),
+                "sweeps": r.sweeps, "diffusion": r.counters.diffusion, "reaction": r.counters.reaction,
+                "newton_iterations": r.counters.newton_iterations, "mg_cycles": r.counters.mg_cycles,
+                "increments": [float(x).hex() for x in incs[: r.sweeps]],
+            }
+            print(name, s, f"{wall:.1f} s", out["runs"][str(s)]["final_sha256"][:16], flush=True)
+            del f
+        path = os.path.join(HERE, f"full_{name}.json")
+        with open(path, "w") as fh:
+            json.dump(out, fh, indent=1)
+        print("wrote", path, flush=True)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--full":
+        full(sys.argv[2:] or ["c3", "c4"])
+        return
     if O.ref_lib() is None:
         raise SystemExit("oracle/_ref not available: build it with make -C oracle ref (needs /root/reference)")
     out = {}

@@ -476,3 +476,52 @@ def test_multigrid_cycle_cap_matches_oracle(gpu, oracle, cap):
             # in N cycles (residual ..., target ...)"
             want = cerr.split("] ", 1)[1].split(" (residual")[0]
             assert gerr == want, (gerr, want)
+
+
+def test_c2_end_to_end_vs_independent_banded_lu(gpu, oracle):
+    """C2 at its full size (N = 65536), 2 steps, every scheme: the GPU's exact circulant scan against
+    the oracle driven with the INDEPENDENT 1-D solver (the ring folded into a band and solved by the
+    restated banded_solve, reference linalg.cpp:105-155) -- not the emulation of the GPU's blocked scan.
+    Bar (north_star): per step max relative difference <= 1e-10 with equal Newton-iteration counts."""
+    spec = P.config_c2(n_steps=2)
+    lu = P.config_c2(n_steps=2).problem
+    lu.diffusion_solver = _abi.DIFFUSION_BANDED_ORACLE
+    for scheme in (0, 1, 2):
+        phi_g = spec.phi0.copy()
+        phi_c = spec.phi0.copy()
+        for step in range(2):
+            o = opts(spec, scheme, steps=1)
+            g = api.integrate(spec.problem, phi_g, o)
+            c, reps, _ = oracle.integrate(lu, phi_c, o)
+            err = relerr(g.final_state, c)
+            assert err <= TOL, (scheme, step, err)
+            assert g.steps[0].counters.newton_iterations == reps[0].counters.newton_iterations, (scheme, step)
+            phi_g, phi_c = g.final_state, c
+
+
+@pytest.mark.parametrize("scheme", [1, 2])
+def test_rhs_exact_zero_skip_with_wild_values(gpu, oracle, scheme):
+    """k_rhs skips the F_A reads of terms whose cE is an exact zero (literal convention) unless an F_A
+    evaluation flagged a value >= 2^1022 / Inf / NaN (Ops::wild).  A state with one huge value
+    (F_A overflows there) must still give the oracle's outcome: the same error, or the same bits
+    (NaN positions included)."""
+    spec = P.config_c3(scale=16, n_steps=1)
+    phi0 = spec.phi0.copy()
+    phi0[1000] = 1e306
+    o = opts(spec, scheme, steps=1)
+    try:
+        c, reps, _ = oracle.integrate(spec.problem, phi0, o)
+        cerr = None
+    except oracle.OracleError as e:
+        cerr = str(e)
+    try:
+        g = api.integrate(spec.problem, phi0, o)
+        gerr = None
+    except api.SolveError as e:
+        gerr = str(e)
+    if cerr is None:
+        assert gerr is None, gerr
+        assert np.array_equal(g.final_state, c, equal_nan=True)
+    else:
+        assert gerr is not None
+        assert cerr.split("] ", 1)[1].split(" (residual")[0] == gerr
