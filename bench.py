@@ -272,6 +272,7 @@ def main():
     lib.cisdc_gpu_kernel_times(ctx.h, None, None, None, 0, 1)  # reset
     lib.cisdc_gpu_device_time_ms(ctx.h, 1)
     newton = 0
+    rexit0 = lib.cisdc_gpu_newton_residual_exits(ctx.h)
     barrier(ws)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
@@ -279,6 +280,11 @@ def main():
             newton += step_device()
         torch.cuda.synchronize()
     barrier(ws)
+    newton_rexits = lib.cisdc_gpu_newton_residual_exits(ctx.h) - rexit0
+    # the same FP64 probe again right after the timed steps: the board is hot and at the clock the
+    # Newton kernel ran at (sustained denominator; the one above ran cold, at boost)
+    pk_fma_s, pk_mul_s = C.c_double(), C.c_double()
+    lib.cisdc_gpu_fp64_peak(C.byref(pk_fma_s), C.byref(pk_mul_s))
     dev_ms = lib.cisdc_gpu_device_time_ms(ctx.h, 1)
     launches = int(lib.cisdc_gpu_launch_count(ctx.h))  # our kernels launched in the timed region
     tmax = max_over_ranks(ws, dev_ms)
@@ -329,17 +335,20 @@ def main():
     dom = max(classes, key=lambda x: x["ms"])
     cell_solves = desc.ncell * spec.M * spec.n_sweeps * args.steps * (spec.nu if scheme == 2 else 1)
     sparse = os.environ.get("CISDC_RTC", "1") != "0"  # the specialised kernel runs the static-pattern LU
-    newton_flops = roofline.newton_work(desc, newton, cell_solves, sparse=sparse)
+    newton_flops = roofline.newton_work(desc, newton, newton - newton_rexits, sparse=sparse)
     if dom["kernel"] == "react_newton" and desc.nspecies >= 9:
         achieved = newton_flops / (dom["ms"] * 1e-3) / 1e12
         # The kernel's arithmetic is the reference's no-FMA operation sequence (bit parity), i.e.
         # DADD / DMUL, one flop per FP64 pipe slot: its attainable peak is the measured DMUL/DADD
         # issue rate; the DFMA rate (two flops per slot) is listed beside it.
-        roof = {"bound": "fp64", "kernel": dom["kernel"], "achieved": achieved, "peak": pk_mul.value,
-                "unit": "TFLOP/s", "frac": achieved / pk_mul.value,
-                "peak_source": "measured DMUL/DADD chain peak on this GPU (cisdc_gpu_fp64_peak)",
-                "peak_dfma": pk_fma.value, "frac_of_dfma_peak": achieved / pk_fma.value, "traffic": None,
-                "work": f"{newton} Newton trips, analytic {newton_flops:.3e} FP64 flops"}
+        roof = {"bound": "fp64", "kernel": dom["kernel"], "achieved": achieved, "peak": pk_mul_s.value,
+                "unit": "TFLOP/s", "frac": achieved / pk_mul_s.value,
+                "peak_source": "measured DMUL/DADD chain peak on this GPU (cisdc_gpu_fp64_peak) right after "
+                               "the timed steps (sustained, same power-capped clock)",
+                "peak_burst": pk_mul.value, "frac_of_burst_peak": achieved / pk_mul.value,
+                "peak_dfma": pk_fma_s.value, "frac_of_dfma_peak": achieved / pk_fma_s.value, "traffic": None,
+                "work": f"{newton} Newton trips ({newton - newton_rexits} with a Jacobian solve), "
+                        f"analytic {newton_flops:.3e} FP64 flops"}
     else:
         achieved = dom["gbs"]
         roof = {"bound": "hbm", "kernel": dom["kernel"], "achieved": achieved, "peak": hbm, "unit": "GB/s",
@@ -361,7 +370,8 @@ def main():
             e["ncu"] = {k: ncu[c["kernel"]].get(k) for k in ("dram_pct", "fp64_pipe_pct", "l1_pct")}
         if c["kernel"] == "react_newton" and desc.nspecies >= 9:
             e["fp64_tflops"] = newton_flops / (c["ms"] * 1e-3) / 1e12
-            e["fp64_frac_dmul_dadd_peak"] = e["fp64_tflops"] / pk_mul.value
+            e["fp64_frac_dmul_dadd_peak"] = e["fp64_tflops"] / pk_mul_s.value
+            e["fp64_frac_burst_peak"] = e["fp64_tflops"] / pk_mul.value
         per_class.append(e)
 
     if rank == 0:
@@ -383,6 +393,7 @@ def main():
             "end_to_end_hbm": {"algorithmic_bytes_per_sweep": 8.0 * n * (7 * spec.M + 4),
                                "achieved_gbs": 8.0 * n * (7 * spec.M + 4) * spec.n_sweeps * args.steps / (tmax * 1e-3) / 1e9},
             "newton_trips_per_cell_solve": newton / max(cell_solves, 1),
+            "newton_residual_exit_fraction": newton_rexits / max(cell_solves, 1),
         }
         clk_s = clk.summary()
         line["clocks"] = clk_s

@@ -77,7 +77,7 @@ enum {
    BANDED_ORACLE: cyclic banded LU (reference banded_solve semantics), CPU oracle only (cross-check) */
 enum { CISDC_DIFFUSION_DIRECT = 0, CISDC_DIFFUSION_MULTIGRID = 1, CISDC_DIFFUSION_BANDED_ORACLE = 2 };
 enum { CISDC_FIELD_PHI = 0, CISDC_FIELD_FA = 1, CISDC_FIELD_FD = 2, CISDC_FIELD_FR = 3, CISDC_FIELD_PHI_AD = 4 };
-enum { CISDC_STAGE_ADVECTION = 0, CISDC_STAGE_DIFFUSION = 1, CISDC_STAGE_REACTION = 2 };
+enum { CISDC_STAGE_ADVECTION = 0, CISDC_STAGE_DIFFUSION = 1, CISDC_STAGE_REACTION = 2, CISDC_STAGE_COUPLED = 3 };
 
 #define CISDC_MAX_M 8
 #define CISDC_MAX_SPECIES 16
@@ -206,6 +206,9 @@ const char* cisdc_gpu_kernel_class_name(int cls);
 double cisdc_gpu_device_time_ms(cisdc_gpu_ctx* ctx, int reset);
 /* kernel launches issued since creation (or the last kernel_times reset) */
 long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx);
+/* cell Newton solves since creation that ended at the residual test |f| <= tol (their last trip
+   built no Jacobian); with newton_iterations this splits the trips for the flop model (bench.py) */
+long long cisdc_gpu_newton_residual_exits(const cisdc_gpu_ctx* ctx);
 /* FP64 pipe peak on the current device: DFMA chains and DMUL+DADD chains, TFLOP/s */
 int cisdc_gpu_fp64_peak(double* tflops_dfma, double* tflops_dmul_dadd);
 /* ---- PMISDC schedule trace (cisdc::CellTrace / ScheduleTrace, pipeline.hpp:72-84) ----

@@ -109,7 +109,9 @@ int co_problem_create(const cisdc_problem_desc* desc, co_problem** out, char* er
     goto fail_;                                          \
   } while (0)
   if (desc->kind == CISDC_PROBLEM_LINEAR_SCALAR) {
-    p->dim = p->ncell = 1;
+    /* n[0] >= 1 independent copies of the scalar model (the reference's dimension-1 problem per
+       element; n[0] = 1 is LinearScalarProblem itself) */
+    p->dim = p->ncell = (size_t)(desc->n[0] >= 1 ? desc->n[0] : 1);
     p->S = 1;
   } else if (desc->kind == CISDC_PROBLEM_REFERENCE_RD) {
     p->nx = desc->n[0];
@@ -1131,7 +1133,7 @@ int co_eval(co_problem* p, int stage, const double* phi, double* out) {
   switch (p->d.kind) {
     case CISDC_PROBLEM_LINEAR_SCALAR: {
       const double c = stage == CISDC_STAGE_ADVECTION ? p->d.ref_a : (stage == CISDC_STAGE_DIFFUSION ? p->d.ref_d : p->d.ref_r);
-      out[0] = c * phi[0];
+      for (size_t i = 0; i < p->dim; ++i) out[i] = c * phi[i];  /* linear.cpp:19-30 per element */
       return CISDC_OK;
     }
     case CISDC_PROBLEM_REFERENCE_RD:
@@ -1160,7 +1162,7 @@ int co_solve(co_problem* p, int stage, double coef, const double* rhs, double* o
         what = "LinearScalarProblem: singular coupled stage";
       }
       if (denom == 0.0) return fail(p, CISDC_E_SOLVE, what);
-      out[0] = rhs[0] / denom;
+      for (size_t i = 0; i < p->dim; ++i) out[i] = rhs[i] / denom;  /* linear.cpp:32-50 per element */
       return CISDC_OK;
     }
     case CISDC_PROBLEM_REFERENCE_RD:

@@ -127,6 +127,7 @@ GPU_SYMBOLS = [
     ("cisdc_gpu_kernel_class_name", C.c_char_p, [C.c_int]),
     ("cisdc_gpu_device_time_ms", C.c_double, [_vp, C.c_int]),
     ("cisdc_gpu_launch_count", C.c_longlong, [_vp]),
+    ("cisdc_gpu_newton_residual_exits", C.c_longlong, [_vp]),
     ("cisdc_gpu_fp64_peak", C.c_int, [_dp, _dp]),
     ("cisdc_rtc_compile_check", C.c_int, [C.POINTER(ProblemDescC), C.c_char_p, C.c_size_t]),
     ("cisdc_gpu_set_trace", C.c_int, [_vp, C.c_int]),

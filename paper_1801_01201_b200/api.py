@@ -251,6 +251,11 @@ class GpuProblem:
     def solve_reaction(self, coef, rhs, counters=None):
         return self._solve(_abi.STAGE_REACTION, coef, rhs, counters)
 
+    def solve_coupled(self, coef, rhs, counters=None):
+        """phi - coef (F_D + F_R)(phi) = rhs (operator_split.hpp:49-50); problems without a coupled solve
+        raise CapabilityError, as in the reference."""
+        return self._solve(_abi.STAGE_COUPLED, coef, rhs, counters)
+
     def close(self):
         self.ctx.close()
 

@@ -119,6 +119,8 @@ struct cisdc_gpu_ctx {
   Reaction rx{};
   int S = 1;
   bool ref_rd = false;
+  bool linear = false;  // CISDC_PROBLEM_LINEAR_SCALAR: (a, d, r) per element, exact stage solves
+  double lin_a = 0.0, lin_d = 0.0, lin_r = 0.0;
   // device memory
   std::vector<void*> allocs;
   double* node0[4] = {};                       // phi0, fa0, fd0, fr0 (shared by both sets)
@@ -149,6 +151,8 @@ struct cisdc_gpu_ctx {
   double* h_incr = nullptr;   // pinned mirror
   int incr_slot = 0;
   unsigned long long newton_seen = 0, mg_seen = 0;
+  unsigned long long newton_res_exits = 0;  // device counter as of the last check_status
+  unsigned long long loop_seen = 0;         // DevStatus::loop_kernels already counted
   cudaStream_t s_main = nullptr, s_r = nullptr;
   int num_sms = 148;
   // PMISDC schedule trace (cisdc_gpu_set_trace / cisdc_gpu_last_trace)
@@ -236,6 +240,13 @@ bool eval_pair() {
 
 int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd, cudaStream_t s) {
   const Geom& g = ctx->g;
+  if (ctx->linear) {
+    ctx->tm.before(kKEvalAD, s);
+    k_lin_eval<<<grid_of(g.n, 256), 256, 0, s>>>(phi, fa, fd, ctx->lin_a, ctx->lin_d, g.n, ctx->ops.wild);
+    ctx->tm.after(kKEvalAD, s, F8(ctx) * (1 + (fa != nullptr) + (fd != nullptr)));
+    CU(cudaGetLastError());
+    return CISDC_OK;
+  }
   const dim3 grid = stencil_grid(g.nx, g.ny, g.nz, g.S, g.ndim), block = stencil_block(g.ndim);
   ctx->tm.before(kKEvalAD, s);
   switch (g.ndim) {
@@ -363,6 +374,8 @@ void launch_fixup_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
 }
 
 int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a_in, cudaStream_t s) {
+  if (ctx->linear && 1.0 - a_in.coef * ctx->lin_r == 0.0)
+    return set_err(ctx, CISDC_E_SOLVE, "LinearScalarProblem: singular reaction stage");
   ReactArgs a = a_in;
   a.tag = next_tag(ctx, CISDC_STAGE_REACTION);
   if (ctx->rtc.ready) {
@@ -498,8 +511,33 @@ int launch_solve1d_e(cisdc_gpu_ctx* ctx, const Solve1dArgs& a, int cl, cudaStrea
   return CISDC_OK;
 }
 
+// LinearScalarProblem stage solves (linear.cpp:32-50): denom = 1 - coef * c, checked here (the
+// reference throws SolveError before touching the output)
+int linear_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rhs, double* out, cudaStream_t s) {
+  double denom;
+  const char* what;
+  if (stage == CISDC_STAGE_DIFFUSION) {
+    denom = 1.0 - coef * ctx->lin_d;
+    what = "LinearScalarProblem: singular diffusion stage";
+  } else if (stage == CISDC_STAGE_REACTION) {
+    denom = 1.0 - coef * ctx->lin_r;
+    what = "LinearScalarProblem: singular reaction stage";
+  } else {
+    denom = 1.0 - coef * (ctx->lin_d + ctx->lin_r);
+    what = "LinearScalarProblem: singular coupled stage";
+  }
+  if (denom == 0.0) return set_err(ctx, CISDC_E_SOLVE, what);
+  const int cls = stage == CISDC_STAGE_REACTION ? kKReact : kKSolve1d;
+  ctx->tm.before(cls, s);
+  k_lin_div<<<grid_of(ctx->g.n, 256), 256, 0, s>>>(rhs, out, denom, ctx->g.n);
+  ctx->tm.after(cls, s, 2.0 * F8(ctx));
+  CU(cudaGetLastError());
+  return CISDC_OK;
+}
+
 int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* out, cudaStream_t s) {
   const long long n = ctx->g.n;
+  if (ctx->linear) return linear_solve(ctx, CISDC_STAGE_DIFFUSION, coef, rhs, out, s);
   if (ctx->ref_rd) {
     if (coef == 0.0) {
       CU(cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
@@ -583,6 +621,9 @@ int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters) {
     counters->mg_cycles += (long long)(h.mg_cycles - ctx->mg_seen);
   }
   ctx->newton_seen = h.newton_trips;
+  ctx->newton_res_exits = h.newton_res_exits;
+  ctx->tm.add_launches((long long)(h.loop_kernels - ctx->loop_seen));
+  ctx->loop_seen = h.loop_kernels;
   ctx->mg_seen = h.mg_cycles;
   ctx->fail_sweep = 0;
   if (h.fail_key != ~0ull) {
@@ -605,6 +646,8 @@ int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters) {
     DevStatus z{};  // reset the status word so the context stays usable
     z.fail_key = ~0ull;
     z.newton_trips = h.newton_trips;
+    z.newton_res_exits = h.newton_res_exits;
+    z.loop_kernels = h.loop_kernels;
     z.mg_cycles = h.mg_cycles;
     CU(cudaMemcpy(ctx->d_st, &z, sizeof(z), cudaMemcpyHostToDevice));
     ctx->tags.clear();
@@ -634,7 +677,7 @@ bool react_fd_separate() {
   return v;
 }
 int prepare_fd_ad(cisdc_gpu_ctx* ctx, ReactArgs& a, cudaStream_t s) {
-  if (!react_fd_separate() || ctx->g.ndim < 2) return CISDC_OK;
+  if (!ctx->linear && (!react_fd_separate() || ctx->g.ndim < 2)) return CISDC_OK;
   a.fd_ad = ctx->fd_ad[1];
   return launch_eval_ad(ctx, a.phi_ad, nullptr, ctx->fd_ad[1], s);
 }
@@ -689,6 +732,50 @@ int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
     TRY(launch_react(ctx, kModeMisdcq, a, s));
     if (c) ++c->reaction;
     TRY(launch_eval_ad(ctx, ctx->own[nxt][kPhi][m + 1], ctx->own[nxt][kFa][m + 1], ctx->own[nxt][kFd][m + 1], s));
+  }
+  return CISDC_OK;
+}
+
+// imexq_sweep (integrators.cpp:145-173): per node, rhs = base + sum_j [cE (fa - fa_p) + cI (fd - fd_p +
+// fr - fr_p)]_j - coef (fd_p + fr_p)_{m+1}, the coupled solve phi - coef (F_D + F_R)(phi) = rhs,
+// phi_AD = phi, and the three evaluations at phi.  Only problems with a coupled solve (the
+// linear scalar model, as in the reference) run it.
+int sweep_imexq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
+  if (!ctx->linear)
+    return set_err(ctx, CISDC_E_CAPABILITY, "imexq_sweep: problem provides no coupled diffusion-reaction solve");
+  const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
+  cudaStream_t s = ctx->s_main;
+  reset_views(ctx, nxt);
+  TRY(launch_quad_base(ctx, prev, dt, s));
+  for (int m = 0; m < M; ++m) {
+    const double coef = dt * QI(ctx->tb, m, m);
+    RhsArgs r{};
+    r.kind = kRhsImexq;
+    r.nt = m;
+    for (int j = 1; j <= m; ++j) {
+      RhsTerm& t = r.t[j - 1];
+      t.cE = dt * QE(ctx->tb, m, j - 1);
+      t.cI = dt * QI(ctx->tb, m, j - 1);
+      t.skipA = t.cE == 0.0;
+      t.A = V(ctx, nxt, kFa, j);
+      t.Ap = V(ctx, prev, kFa, j);
+      t.D = V(ctx, nxt, kFd, j);
+      t.Dp = V(ctx, prev, kFd, j);
+      t.R = V(ctx, nxt, kFr, j);
+      t.Rp = V(ctx, prev, kFr, j);
+    }
+    r.fc = coef;
+    r.X = V(ctx, prev, kFd, m + 1);
+    r.Y = V(ctx, prev, kFr, m + 1);
+    r.base = ctx->base[m];
+    r.out = ctx->rhs_d;
+    TRY(launch_rhs(ctx, r, s));
+    double* phi = ctx->own[nxt][kPhi][m + 1];
+    TRY(linear_solve(ctx, CISDC_STAGE_COUPLED, coef, ctx->rhs_d, phi, s));
+    if (c) ++c->coupled;
+    CU(cudaMemcpyAsync(ctx->phi_ad[m + 1], phi, sizeof(double) * ctx->g.n, cudaMemcpyDeviceToDevice, s));
+    TRY(launch_eval_ad(ctx, phi, ctx->own[nxt][kFa][m + 1], ctx->own[nxt][kFd][m + 1], s));
+    TRY(launch_eval_r(ctx, phi, ctx->own[nxt][kFr][m + 1], s));
   }
   return CISDC_OK;
 }
@@ -986,8 +1073,7 @@ int run_one_sweep(cisdc_gpu_ctx* ctx, int scheme, double dt, int nu, int workers
     case CISDC_SCHEME_MISDC: TRY(sweep_misdc(ctx, dt, c)); break;
     case CISDC_SCHEME_MISDCQ: TRY(sweep_misdcq(ctx, dt, c)); break;
     case CISDC_SCHEME_CISDCQ: TRY(sweep_cisdcq(ctx, dt, nu, workers, c)); break;
-    case CISDC_SCHEME_IMEXQ:
-      return set_err(ctx, CISDC_E_CAPABILITY, "imexq_sweep: problem provides no coupled diffusion-reaction solve");
+    case CISDC_SCHEME_IMEXQ: TRY(sweep_imexq(ctx, dt, c)); break;
     default: return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown scheme");
   }
   const int nxt = 1 - prev;
@@ -1019,6 +1105,9 @@ extern "C" {
 const char* cisdc_gpu_last_error(const cisdc_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 size_t cisdc_gpu_dimension(const cisdc_gpu_ctx* ctx) { return ctx ? (size_t)ctx->g.n : 0; }
 long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx) { return ctx ? ctx->tm.launches : 0; }
+long long cisdc_gpu_newton_residual_exits(const cisdc_gpu_ctx* ctx) {
+  return ctx ? (long long)ctx->newton_res_exits : 0;
+}
 
 void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
   if (!ctx) return;
@@ -1143,7 +1232,19 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
       return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "diffusion solver not available on the GPU (oracle-only)");
     }
   } else if (d->kind == CISDC_PROBLEM_LINEAR_SCALAR) {
-    return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "linear scalar problem is oracle-only (dimension 1)");
+    // LinearScalarProblem (linear.hpp:31-51): n[0] >= 1 independent copies (n[0] = 1 is the
+    // reference's dimension-1 problem); the only problem class with the coupled solve IMEXQ needs
+    ctx->linear = true;
+    g.nx = d->n[0] >= 1 ? d->n[0] : 1;
+    g.ny = g.nz = 1;
+    g.ndim = 1;
+    g.S = 1;
+    ctx->lin_a = d->ref_a;
+    ctx->lin_d = d->ref_d;
+    ctx->lin_r = d->ref_r;
+    rx.kind = kReactLinear;
+    rx.lambda = d->ref_r;
+    rx.max_iter = 1;
   } else {
     return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "unknown problem kind");
   }
@@ -1187,7 +1288,7 @@ static int build_ctx(cisdc_gpu_ctx* ctx, const cisdc_problem_desc* d, const cisd
     ctx->defer_count = reinterpret_cast<int*>(ctx->defer_list + g.ncell);
     CU(cudaMemset(ctx->defer_count, 0, sizeof(int)));
   }
-  if (!ctx->ref_rd && d->diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
+  if (!ctx->ref_rd && !ctx->linear && d->diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
     const int rc = mg_init(ctx->mg, g, *d);
     if (rc) return set_err(ctx, rc, "multigrid: hierarchy setup failed (" + std::to_string(rc) + ")");
   }
@@ -1358,6 +1459,8 @@ int cisdc_gpu_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rh
     a.phi_out = ctx->scratch;
     a.fr_out = nullptr;
     TRY(launch_react(ctx, kModePlain, a, s));
+  } else if (ctx->linear) {
+    TRY(linear_solve(ctx, CISDC_STAGE_COUPLED, coef, ctx->rhs_d, ctx->scratch, s));
   } else {
     return set_err(ctx, CISDC_E_CAPABILITY, "OperatorSplitProblem: coupled diffusion-reaction solve not provided");
   }

@@ -31,7 +31,8 @@ struct DevStatus {
   unsigned long long fail_key;        // ~0ull if nothing failed
   unsigned long long newton_trips;    // Newton residual evaluations (atomicAdd)
   unsigned long long mg_cycles;       // multigrid V-cycles
-  double incr_partial_unused;
+  unsigned long long newton_res_exits;  // cell solves that ended at the residual test (atomicAdd)
+  unsigned long long loop_kernels;      // kernels run by device-looped multigrid cycles (multigrid.cuh)
 };
 
 #ifdef __CUDACC__

@@ -59,6 +59,17 @@ struct MgHierarchy {
     long long kernels;
   };
   std::vector<CycleGraph> graphs;
+  // Device-looped solves (mg_solve_graph): the first cycle, a WHILE node whose body is one cycle
+  // (its decision kernel sets the condition), and the copy for species that needed no cycle.
+  struct SolveGraph {
+    double coef;
+    const void *rhs, *out;
+    int L;
+    cudaGraphExec_t exec;
+    long long kernels;  // launched by every replay (the body's cycles are counted on the device)
+  };
+  std::vector<SolveGraph> solve_graphs;
+  cudaStream_t s_body = nullptr;  // capture stream of the WHILE bodies
   std::vector<void*> allocs;
 };
 
@@ -161,10 +172,10 @@ __global__ void k_mg_copy_unswept(const double* __restrict__ b, double* __restri
 
 // per-species stop decision of the oracle's loop: rn <= tol*bn -> done; cap -> failure
 // count == 0: the decision of a check-only pass (no cycle follows it in the same launch sequence;
-// the next cycle's fused check repeats the same decision and counts)
-__global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int* cycles, const double* bmax,
-                            double* rmax, int* flag, DevStatus* st, const unsigned* tag, int count = 1) {
-  if (threadIdx.x != 0) return;
+// the next cycle's fused check repeats the same decision and counts).  Returns "some species goes on".
+__device__ __forceinline__ int mg_update_body(int S, double tol, int max_cycles, int* active, int* cycles,
+                                              const double* bmax, double* rmax, int* flag, DevStatus* st,
+                                              const unsigned* tag, int count) {
   int any = 0;
   for (int s = 0; s < S; ++s) {
     if (!active[s]) continue;
@@ -189,6 +200,25 @@ __global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int*
   }
   for (int s = 0; s < S; ++s) rmax[s] = 0.0;
   flag[0] = any;
+  return any;
+}
+__global__ void k_mg_update(int S, double tol, int max_cycles, int* active, int* cycles, const double* bmax,
+                            double* rmax, int* flag, DevStatus* st, const unsigned* tag, int count = 1) {
+  if (threadIdx.x != 0) return;
+  mg_update_body(S, tol, max_cycles, active, cycles, bmax, rmax, flag, st, tag, count);
+}
+// The same decision inside a device-looped solve graph (mg_solve_graph): it also sets the WHILE
+// node's condition -- run another cycle iff some species goes on and none failed, the host loop's
+// exit test -- and counts the kernels of that next cycle into the status word (the host learns
+// the launch count at the step's status read).
+__global__ void k_mg_update_loop(int S, double tol, int max_cycles, int* active, int* cycles, const double* bmax,
+                                 double* rmax, int* flag, DevStatus* st, const unsigned* tag,
+                                 cudaGraphConditionalHandle loop, unsigned long long cycle_kernels) {
+  if (threadIdx.x != 0) return;
+  const int any = mg_update_body(S, tol, max_cycles, active, cycles, bmax, rmax, flag, st, tag, 1);
+  const unsigned go = (any && flag[1] == 0) ? 1u : 0u;
+  if (go) st->loop_kernels += cycle_kernels;
+  cudaGraphSetConditional(loop, go);
 }
 
 // per-solve reset of the bookkeeping (one launch instead of memsets and a host copy); the solve's
@@ -750,12 +780,17 @@ inline int mg_init(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d) {
   if (!h.d_active || !h.d_cycles || !h.d_bmax || !h.d_rmax || !h.d_flag || !h.d_tag) return CISDC_E_CUDA;
   if (cudaMallocHost(&v, sizeof(int) * 2) != cudaSuccess) return CISDC_E_CUDA;
   h.h_flag = static_cast<int*>(v);
+  if (cudaStreamCreateWithFlags(&h.s_body, cudaStreamNonBlocking) != cudaSuccess) return CISDC_E_CUDA;
   return CISDC_OK;
 }
 
 inline void mg_free(MgHierarchy& h) {
   for (auto& g : h.graphs) cudaGraphExecDestroy(g.exec);
   h.graphs.clear();
+  for (auto& g : h.solve_graphs) cudaGraphExecDestroy(g.exec);
+  h.solve_graphs.clear();
+  if (h.s_body) cudaStreamDestroy(h.s_body);
+  h.s_body = nullptr;
   for (void* p : h.allocs) cudaFree(p);
   h.allocs.clear();
   if (h.h_flag) cudaFreeHost(h.h_flag);
@@ -898,11 +933,20 @@ struct MgRunner {
   dim3 grid(const MgLevel& Lv) const { return stencil_grid(Lv.nx, Lv.ny, Lv.nz, h.S, DIM); }
   dim3 block() const { return stencil_block(DIM); }
 
+  // device-looped solve graph being captured (mg_solve_graph): decisions also drive the WHILE node
+  bool loop = false;
+  cudaGraphConditionalHandle loop_handle{};
+  unsigned long long loop_cycle_kernels = 0;
+
   // per-species decision of the oracle's loop on the reduced norms (enables the rest of the cycle)
   void update(int count = 1) {
     hook->before(kKMgNorm, s);
-    k_mg_update<<<1, 32, 0, s>>>(h.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
-                                 h.d_flag, st, h.d_tag, count);
+    if (loop)
+      k_mg_update_loop<<<1, 32, 0, s>>>(h.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
+                                        h.d_flag, st, h.d_tag, loop_handle, loop_cycle_kernels);
+    else
+      k_mg_update<<<1, 32, 0, s>>>(h.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
+                                   h.d_flag, st, h.d_tag, count);
     hook->after(kKMgNorm, s, 0.0);
   }
 
@@ -1094,6 +1138,107 @@ inline MgHierarchy::CycleGraph* cycle_graph(MgHierarchy& h, MgRunner<DIM>& R, do
   return &h.graphs.back();
 }
 
+// Device-side convergence loops for fused-check solves (CISDC_MG_LOOP=1).  Off by default: measured
+// on B200 (profiles/r2/r2d_*), the loop removes the per-solve host wait but gives up the predicted
+// residual-only last check (a WHILE body cannot know which check is the last), and the host wait
+// was already hidden behind the batches it enqueues: C5 549.4 -> 552.6 ms per step, C4 117.7 ->
+// 119.7, C3 35.61 -> 35.57.  It is the form a graph-captured sweep needs (no host decision inside).
+inline bool mg_loop_enabled() {  // read per solve, so a process can switch it (tests do)
+  const char* e = std::getenv("CISDC_MG_LOOP");
+  return e && e[0] == '1';
+}
+
+// The whole solve as one graph, cached per (coef, rhs, out, L): the first cycle (check of x = b and
+// ||b||, sweeps from b), a WHILE node whose body is one checking cycle -- its decision kernel
+// (k_mg_update_loop) sets the condition to the host loop's "go on" test -- and the copy of b for
+// species that met the tolerance at x = b.  The host enqueues k_mg_begin + one graph launch and
+// never waits: no per-solve synchronisation, and the cycle count is whatever the device decides
+// (the oracle's loop exactly; the cap is the decision kernel's).  R must be in its pre-solve state
+// (level-0 x = out, first_x = rhs); the capture launches nothing.  nullptr if capture fails.
+template <int DIM>
+inline MgHierarchy::SolveGraph* mg_solve_graph(MgHierarchy& h, MgRunner<DIM>& R, const Geom& g, double coef,
+                                               const double* rhs, double* out, cudaStream_t s) {
+  for (auto& e : h.solve_graphs)
+    if (e.coef == coef && e.rhs == rhs && e.out == out && e.L == R.L) return &e;
+  CountingHook counter;
+  LaunchHook* saved = R.hook;
+  R.hook = &counter;
+  auto reset = [&]() {
+    R.first_x = rhs;
+    R.check_next = true;
+    R.first_check = true;
+    R.recording = false;
+  };
+  // kernels of one cycle (a throwaway capture of the same launch sequence)
+  reset();
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    R.hook = saved;
+    return nullptr;
+  }
+  R.vcycle(0);
+  cudaGraph_t tmp = nullptr;
+  cudaError_t e = cudaStreamEndCapture(s, &tmp);
+  if (tmp) cudaGraphDestroy(tmp);
+  const long long per_cycle = counter.n;
+  cudaGraph_t graph = nullptr;
+  cudaGraphConditionalHandle hnd{};
+  bool ok = e == cudaSuccess && cudaGraphCreate(&graph, 0) == cudaSuccess &&
+            cudaGraphConditionalHandleCreate(&hnd, graph, 0, cudaGraphCondAssignDefault) == cudaSuccess;
+  if (ok) ok = cudaStreamBeginCaptureToGraph(s, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) ==
+               cudaSuccess;
+  if (ok) {
+    reset();
+    R.loop = true;
+    R.loop_handle = hnd;
+    R.loop_cycle_kernels = (unsigned long long)per_cycle;
+    R.vcycle(0);  // the first cycle
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    cudaGraph_t cg = nullptr;
+    cudaGraphNode_t wnode = nullptr;
+    cudaGraphNodeParams p{};
+    p.type = cudaGraphNodeTypeConditional;
+    p.conditional.handle = hnd;
+    p.conditional.type = cudaGraphCondTypeWhile;
+    p.conditional.size = 1;
+    ok = cudaStreamGetCaptureInfo(s, &cs, nullptr, &cg, &deps, &nd) == cudaSuccess &&
+         cudaGraphAddNode(&wnode, cg, deps, nd, &p) == cudaSuccess;
+    if (ok) {  // the body: one checking cycle, captured on the body stream
+      const cudaStream_t s_saved = R.s;
+      R.s = h.s_body;
+      ok = cudaStreamBeginCaptureToGraph(h.s_body, p.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        R.check_next = true;
+        R.vcycle(0);
+        cudaGraph_t bg = nullptr;
+        ok = cudaStreamEndCapture(h.s_body, &bg) == cudaSuccess;
+      }
+      R.s = s_saved;
+      ok = ok && cudaStreamUpdateCaptureDependencies(s, &wnode, 1, cudaStreamSetCaptureDependencies) == cudaSuccess;
+    }
+    // species that met the tolerance at x = b: out = b (the kernel reads the cycle counts)
+    const dim3 cgrid((unsigned)std::min<long long>((g.ncell + 255) / 256, 4096), (unsigned)g.S, 1);
+    k_mg_copy_unswept<<<cgrid, 256, 0, s>>>(rhs, out, g.ncell, h.d_cycles);
+    cudaGraph_t done = nullptr;
+    ok = (cudaStreamEndCapture(s, &done) == cudaSuccess) && ok && done == graph;
+  }
+  R.loop = false;
+  R.hook = saved;
+  cudaGraphExec_t exec = nullptr;
+  if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+  if (graph) cudaGraphDestroy(graph);
+  cudaGetLastError();
+  if (!ok) return nullptr;
+  if (h.solve_graphs.size() >= 64) {
+    cudaGraphExecDestroy(h.solve_graphs.front().exec);
+    h.solve_graphs.erase(h.solve_graphs.begin());
+  }
+  h.solve_graphs.push_back({coef, rhs, out, R.L, exec, per_cycle + 1});
+  return &h.solve_graphs.back();
+}
+
 // The oracle's loop per species: x = b; while (||b - A x|| > tol ||b||) { cap check; V-cycle }.
 // Device form: every enqueued V-cycle starts with a level-0 sweep that also reduces the residual
 // norm of its input iterate (k_mg3_tiled<.., NORM> / k_mg_smooth<.., NORM>), followed by the
@@ -1151,6 +1296,19 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     x_check = L0.x;
     R.update();
   };
+  if (fused && mg_loop_enabled() && !hook->timing()) {
+    MgHierarchy::SolveGraph* sg = mg_solve_graph<DIM>(h, R, g, coef, rhs, out, s);
+    if (sg) {
+      if (cudaGraphLaunch(sg->exec, s) != cudaSuccess) return CISDC_E_CUDA;
+      hook->add_launches(sg->kernels);
+      L0.x = own_x;
+      L0.t = own_t;
+      return cudaGetLastError() == cudaSuccess ? CISDC_OK : CISDC_E_CUDA;
+    }
+    R.first_x = rhs;  // capture unavailable: the host-driven loop below
+    R.check_next = false;
+    R.first_check = true;
+  }
   int batch = 1;
   for (const auto& pc : h.predicted)
     if (pc.first == coef) batch = std::max(1, pc.second);

@@ -79,7 +79,8 @@ struct RhsTerm {
 enum RhsKind {
   kRhsMisdcq = 0,  // out = base + sum(AD terms) - fc*X ; out2 = base + sum(ADR terms)
   kRhsCisdcq = 1,  // out = base + sum(ADR terms) + (fc*(X - Y) - fc*Z)
-  kRhsMisdc = 2    // base = phi_m + sum_j sc_j*(fa+fd+fr)_j ; out = base + fc*(X - Y - Z)
+  kRhsMisdc = 2,   // base = phi_m + sum_j sc_j*(fa+fd+fr)_j ; out = base + fc*(X - Y - Z)
+  kRhsImexq = 3    // out = base + sum(ADR terms) - fc*(X + Y)   (imexq_sweep, integrators.cpp:155-164)
 };
 
 struct RhsArgs {
@@ -121,6 +122,19 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
   }
   const bool tame = a.wild == nullptr || *a.wild == 0;
   const double base = a.base[e];
+  if (a.kind == kRhsImexq) {  // the MISDCQ reaction-stage sum, then rhs -= coef * (fd_p + fr_p)
+    double rr = base;
+#pragma unroll
+    for (int t = 0; t < kMaxM; ++t) {
+      if (t >= a.nt) break;
+      const RhsTerm& T = a.t[t];
+      const double tI2 = T.cI * (T.D[e] - T.Dp[e] + T.R[e] - T.Rp[e]);
+      rr += rhs_term_a(T, e, tI2, T.skipA && tame);
+    }
+    rr -= a.fc * (a.X[e] + a.Y[e]);
+    a.out[e] = rr;
+    return;
+  }
   if (a.kind == kRhsMisdcq) {
     double rd = base, rr = base;
 #pragma unroll
@@ -173,6 +187,28 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
   }
   r += a.fc * (a.X[e] - a.Y[e]) - a.fc * a.Z[e];
   a.out[e] = r;
+}
+
+// LinearScalarProblem (proj/core/src/problems/linear.cpp:19-50), per element of a batch of
+// independent copies: F_A = a phi, F_D = d phi (either output may be null), and the exact stage
+// solves out = rhs / denom with denom = 1 - coef * (d | r | d + r) formed and checked on the host.
+__global__ void __launch_bounds__(256) k_lin_eval(const double* __restrict__ phi, double* __restrict__ fa,
+                                                  double* __restrict__ fd, double a, double d, long long n,
+                                                  int* wild) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const double v = phi[e];
+  if (fa) {
+    const double va = a * v;
+    fa[e] = va;
+    flag_wild(wild, wild_bits(va));  // F_A values k_rhs's exact-zero shortcut must not skip
+  }
+  if (fd) fd[e] = d * v;
+}
+__global__ void __launch_bounds__(256) k_lin_div(const double* __restrict__ rhs, double* __restrict__ out,
+                                                 double denom, long long n) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) out[e] = rhs[e] / denom;
 }
 
 constexpr int kIncrBlocks = 1184;  // 8 x 148 SMs; fixed so the reduction tree is fixed

@@ -305,6 +305,9 @@ def config_c5(scale: int = 1, seed: int = 5, n_steps: int = 1) -> RunSpec:
 CONFIGS = {"c0": config_c0, "c1": config_c1, "c2": config_c2, "c3": config_c3, "c4": config_c4, "c5": config_c5}
 
 
-def linear_scalar(a: float, d: float, r: float) -> ProblemDesc:
-    return ProblemDesc(kind=_abi.PROBLEM_LINEAR_SCALAR, ndim=1, n=(1, 1, 1), ref_a=a, ref_d=d, ref_r=r,
+def linear_scalar(a: float, d: float, r: float, batch: int = 1) -> ProblemDesc:
+    """LinearScalarProblem (proj/core/include/cisdc/problems/linear.hpp:31-51): phi' = (a + d + r) phi
+    with exact stage solves and the coupled solve IMEXQ needs; `batch` independent copies (one per
+    element, batch = 1 is the reference's dimension-1 problem)."""
+    return ProblemDesc(kind=_abi.PROBLEM_LINEAR_SCALAR, ndim=1, n=(batch, 1, 1), ref_a=a, ref_d=d, ref_r=r,
                        name="linear")

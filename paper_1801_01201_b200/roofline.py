@@ -88,8 +88,9 @@ def newton_flops(desc, sparse: bool = True) -> tuple[float, float]:
     return float(residual), float(jac + shift + lu + back + update)
 
 
-def newton_work(desc, trips: int, cell_solves: int, sparse: bool = True) -> float:
-    """Lower-bound FP64 flops of `trips` Newton trips over `cell_solves` per-cell solves (each solve's
-    last trip is counted as residual-only)."""
+def newton_work(desc, trips: int, full_trips: int, sparse: bool = True) -> float:
+    """Lower-bound FP64 flops of `trips` Newton trips, `full_trips` of which built and solved the
+    Jacobian (the others ended at the residual test |f| <= tol; the device counts those exits,
+    cisdc_gpu_newton_residual_exits).  Every trip evaluates the residual."""
     res, full = newton_flops(desc, sparse)
-    return trips * res + max(trips - cell_solves, 0) * full
+    return trips * res + max(full_trips, 0) * full

@@ -122,7 +122,7 @@ def main():
                                 "dram_pct": r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                                 "fp64_pipe_pct": r.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                                 "l1_pct": r.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
-                                "source": f"profiles/r1/{tag}_{cfg}_{part}_raw.csv (first captured launch)"}
+                                "source": f"profiles/{tag[:2]}/{tag}_{cfg}_{part}_raw.csv.gz (first captured launch)"}
     lines.append("")
     name = f"{tag}_summary.md" if cfg == "c5" else f"{tag}_{cfg}_summary.md"
     with open(os.path.join(here, name), "w") as f:

@@ -532,3 +532,24 @@ def test_rhs_exact_zero_skip_with_wild_values(gpu, oracle, scheme):
     else:
         assert gerr is not None
         assert cerr.split("] ", 1)[1].split(" (residual")[0] == gerr
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_device_looped_multigrid_bitwise(gpu, oracle, name, monkeypatch):
+    """CISDC_MG_LOOP=1: every multigrid solve is one CUDA graph whose WHILE node runs the V-cycles until
+    the decision kernel (k_mg_update_loop) stops it -- no host synchronisation per solve.  Same cycles,
+    same bits and counts as the oracle (and as the host-driven loop)."""
+    monkeypatch.setenv("CISDC_MG_LOOP", "1")
+    make, steps, schemes = CASES[name]
+    spec = make()
+    for scheme in schemes:
+        _, g, c = per_step_compare(oracle, spec, scheme, steps)
+        assert np.array_equal(g, c), f"{name} scheme {scheme}: not bitwise"
+
+
+@pytest.mark.parametrize("cap", [17, 18, 20])
+def test_device_looped_multigrid_cap(gpu, oracle, cap, monkeypatch):
+    """The cycle cap inside the device loop: the decision kernel flags the failure and ends the WHILE
+    loop; the error text equals the oracle's, a run within the cap is bitwise equal."""
+    monkeypatch.setenv("CISDC_MG_LOOP", "1")
+    test_multigrid_cycle_cap_matches_oracle(gpu, oracle, cap)

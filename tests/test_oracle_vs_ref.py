@@ -96,3 +96,19 @@ def test_reference_initial_condition_matches_config0(ref):
     out = np.empty(200)
     ref.ref_lib().ref_rd_initial_condition(200, 1.0, 2.0, 4.0, out.ctypes.data_as(C.POINTER(C.c_double)))
     assert np.array_equal(out, spec.phi0)
+
+
+@pytest.mark.parametrize("scheme", [0, 1, 2, 3])
+def test_linear_batch_oracle_vs_reference_per_element(ref, scheme):
+    """The oracle's batched LinearScalarProblem (n[0] independent copies, the GPU engine's layout) equals
+    the unmodified reference's dimension-1 integrate element by element; scheme 3 is IMEXQ with the
+    coupled solve (integrators.cpp:145-173, linear.cpp:45-50)."""
+    from paper_1801_01201_b200 import api, problems as P
+    tri = (0.5, -40.0, -3.0)
+    phi0 = np.linspace(-1.5, 2.0, 7)
+    o = api.IntegrateOptions(scheme=scheme, dt=0.05, n_steps=2, M=3, n_sweeps=4, nu=2)
+    c, reps, _ = ref.integrate(P.linear_scalar(*tri, batch=phi0.size), phi0, o)
+    for i in range(phi0.size):
+        r, rreps, _ = ref.ref_integrate(P.linear_scalar(*tri), phi0[i:i + 1], o)
+        assert c[i] == r[0]
+        assert reps[-1].counters.coupled == rreps[-1].counters.coupled
