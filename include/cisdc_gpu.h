@@ -209,6 +209,33 @@ long long cisdc_gpu_launch_count(const cisdc_gpu_ctx* ctx);
 /* cell Newton solves since creation that ended at the residual test |f| <= tol (their last trip
    built no Jacobian); with newton_iterations this splits the trips for the flop model (bench.py) */
 long long cisdc_gpu_newton_residual_exits(const cisdc_gpu_ctx* ctx);
+/* ---- batched iteration-matrix scans (analysis.hpp:72-95; analysis.cpp:215-293) ----------------
+   cisdc::spectral_radius_scan on the GPU, one thread per point: for every scheme, every nu of
+   nu_list (CISDCQ only; 1 otherwise) and every r of r_grid, in that order, the affine iteration
+   matrix G of one sweep on the linear model (a, d, r) -- d = r / 2 (d_rule 0, DRule::half_of_r) or
+   fixed_d (d_rule 1) -- and its spectral radius.  A point whose stage factor vanishes, whose G is
+   not finite, or whose QR iteration reaches its cap gets ok = 0 (gamma 0), as the reference records
+   it.  G_out (optional): the n_points M x M matrices, row-major.  Empty schemes / r_grid ->
+   CISDC_E_INVALID_ARGUMENT with the reference's message (cisdc_last_error). */
+typedef struct cisdc_scan_point {
+  int scheme, M, nu;
+  double a, d, r, dt;
+  double gamma;
+  int ok;
+} cisdc_scan_point;
+int cisdc_gpu_spectral_radius_scan(const int* schemes, int n_schemes, const int* nu_list, int n_nu,
+                                   const double* r_grid, int n_r, int d_rule, double fixed_d, double a, double dt,
+                                   int M, int convention, cisdc_scan_point* out, size_t cap, size_t* n_out,
+                                   double* G_out);
+/* cisdc::spectral_radius (linalg.cpp:197-332) of `count` n x n matrices (row-major, n <= 8), one GPU
+   thread each: rho[i], status[i] = 0 ok, 1 non-finite entry (std::invalid_argument), 2 QR iteration
+   cap (cisdc::NumericError) */
+int cisdc_gpu_spectral_radius_batch(const double* A, int n, int count, double* rho, int* status);
+/* cisdc::log_r_grid (analysis.cpp:255-266): -10^e for n + 1 exponents from lo_exp to hi_exp,
+   n = round((hi - lo) * points_per_decade); returns the count (or -1: points_per_decade < 1) */
+int cisdc_log_r_grid(double lo_exp, double hi_exp, int points_per_decade, double* out, size_t cap);
+const char* cisdc_last_error(void);
+
 /* FP64 pipe peak on the current device: DFMA chains and DMUL+DADD chains, TFLOP/s */
 int cisdc_gpu_fp64_peak(double* tflops_dfma, double* tflops_dmul_dadd);
 /* ---- PMISDC schedule trace (cisdc::CellTrace / ScheduleTrace, pipeline.hpp:72-84) ----

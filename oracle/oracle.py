@@ -26,6 +26,7 @@ REF_SRC = "/root/reference/proj/core"
 _dp = C.POINTER(C.c_double)
 _vp = C.c_void_p
 _cp = C.c_char_p
+_ip = C.POINTER(C.c_int)
 
 _oracle = None
 _ref = None
@@ -127,6 +128,11 @@ def ref_lib() -> C.CDLL | None:
         lib.ref_write_field_snapshot.argtypes = [C.c_char_p, C.c_int, C.c_double, _dp, C.c_size_t, _cp]
         lib.ref_read_field_snapshot.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), _dp,
                                                 C.c_size_t, _cp]
+        lib.ref_spectral_radius.argtypes = [_dp, C.c_int, _dp]
+        sp = C.POINTER(_abi.ScanPointC)
+        lib.ref_spectral_radius_scan.argtypes = [_ip, C.c_int, _ip, C.c_int, _dp, C.c_int, C.c_int, C.c_double,
+                                                 C.c_double, C.c_double, C.c_int, C.c_int, sp, C.c_size_t,
+                                                 C.POINTER(C.c_size_t), _dp, _cp]
         tp = C.POINTER(_abi.CellTraceC)
         lib.ref_validate_trace.argtypes = [C.c_int, C.c_int, C.c_int, tp, C.c_int, _cp, C.c_size_t]
         _ref = lib
@@ -343,3 +349,31 @@ def ref_validate_schedule_trace(M: int, nu: int, trace) -> str:
     if rc:
         raise OracleError(rc, msg.value.decode())
     return msg.value.decode()
+
+
+def ref_spectral_radius_scan(schemes, nu_list, r_grid, d_rule=0, fixed_d=-5.0, a=1.0, dt=1.0, M=4, convention=0,
+                             want_G=False):
+    """The unmodified reference's spectral_radius_scan: (points, G or None)."""
+    sch = np.ascontiguousarray(schemes, dtype=np.int32)
+    nus = np.ascontiguousarray(nu_list if len(nu_list) else [1], dtype=np.int32)
+    rg = np.ascontiguousarray(r_grid, dtype=np.float64)
+    cap = max(len(sch) * max(len(nus), 1) * max(len(rg), 1), 1)
+    out = (_abi.ScanPointC * cap)()
+    n = C.c_size_t()
+    G = np.zeros(cap * M * M) if want_G else None
+    err = C.create_string_buffer(1024)
+    rc = ref_lib().ref_spectral_radius_scan(sch.ctypes.data_as(_ip), len(sch), nus.ctypes.data_as(_ip), len(nu_list),
+                                            _dp_of(rg) if len(rg) else None, len(rg), d_rule, fixed_d, a, dt, M,
+                                            convention, out, cap, C.byref(n), _dp_of(G) if want_G else None, err)
+    if rc:
+        raise OracleError(rc, err.value.decode())
+    pts = [out[i] for i in range(n.value)]
+    return pts, (G[: n.value * M * M].reshape(n.value, M, M) if want_G else None)
+
+
+def ref_spectral_radius(A):
+    """The unmodified reference's spectral_radius of one square matrix: (rho, error code)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    rho = C.c_double(0.0)
+    rc = ref_lib().ref_spectral_radius(_dp_of(A), A.shape[0], C.byref(rho))
+    return rho.value, rc

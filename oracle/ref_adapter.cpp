@@ -21,6 +21,7 @@
 #include <string>
 #include <vector>
 
+#include "cisdc/analysis.hpp"
 #include "cisdc/errors.hpp"
 #include "cisdc/integrators.hpp"
 #include "cisdc/linalg.hpp"
@@ -330,6 +331,67 @@ int ref_validate_trace(int M, int nu, int workers, const cisdc_cell_trace* cells
     return CISDC_OK;
   } catch (const std::exception& e) {
     std::snprintf(msg, cap, "%s", e.what());
+    return code_of(e);
+  }
+}
+
+// cisdc::spectral_radius (linalg.cpp:197-332) of one n x n row-major matrix
+int ref_spectral_radius(const double* A, int n, double* rho) {
+  try {
+    cisdc::DenseMatrix M(n, n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) M(i, j) = A[i * n + j];
+    *rho = cisdc::spectral_radius(M);
+    return CISDC_OK;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// cisdc::spectral_radius_scan (analysis.cpp:270-293) with the C-ABI's point layout; G_out
+// (optional) receives affine_iteration_matrix(...).G of every point that has one (zeros otherwise).
+int ref_spectral_radius_scan(const int* schemes, int n_schemes, const int* nu_list, int n_nu, const double* r_grid,
+                             int n_r, int d_rule, double fixed_d, double a, double dt, int M, int convention,
+                             cisdc_scan_point* out, size_t cap, size_t* n_out, double* G_out, char* err) {
+  try {
+    cisdc::ScanOptions o;
+    for (int i = 0; i < n_schemes; ++i) o.schemes.push_back(static_cast<cisdc::Scheme>(schemes[i]));
+    for (int i = 0; i < n_nu; ++i) o.nu_list.push_back(nu_list[i]);
+    for (int i = 0; i < n_r; ++i) o.r_grid.push_back(r_grid[i]);
+    o.d_rule = d_rule == 0 ? cisdc::DRule::half_of_r : cisdc::DRule::fixed;
+    o.fixed_d = fixed_d;
+    o.a = a;
+    o.dt = dt;
+    o.M = M;
+    o.convention = conv_of(convention);
+    const std::vector<cisdc::ScanPoint> pts = cisdc::spectral_radius_scan(o);
+    if (n_out) *n_out = pts.size();
+    if (cap < pts.size()) return CISDC_E_INVALID_ARGUMENT;
+    for (size_t i = 0; i < pts.size(); ++i) {
+      const cisdc::ScanPoint& p = pts[i];
+      out[i] = cisdc_scan_point{static_cast<int>(p.scheme), p.M, p.nu, p.a, p.d, p.r, p.dt, p.gamma, p.ok ? 1 : 0};
+      if (G_out) {
+        double* g = G_out + i * (size_t)M * M;
+        std::memset(g, 0, sizeof(double) * M * M);
+        try {
+          const cisdc::IterationMatrixResult res =
+              cisdc::affine_iteration_matrix(p.scheme, {p.a, p.d, p.r}, p.dt, p.M, p.nu, o.convention);
+          for (int r = 0; r < M; ++r)
+            for (int c = 0; c < M; ++c) g[r * M + c] = res.G(r, c);
+        } catch (const std::exception&) {
+          // singular stage / non-finite G / QR cap: the point is ok = false; G where it exists
+          try {
+            const cisdc::AffineMap mp = cisdc::affine_sweep_map(p.scheme, {p.a, p.d, p.r}, p.dt, p.M, p.nu, o.convention);
+            for (int r = 0; r < M; ++r)
+              for (int c = 0; c < M; ++c) g[r * M + c] = mp.W(r, c);
+          } catch (const std::exception&) {
+          }
+        }
+      }
+    }
+    return CISDC_OK;
+  } catch (const std::exception& e) {
+    if (err) std::snprintf(err, 1024, "%s", e.what());
     return code_of(e);
   }
 }

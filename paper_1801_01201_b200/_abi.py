@@ -103,6 +103,14 @@ class CellTraceC(C.Structure):
                 ("seq_start", C.c_longlong), ("seq_end", C.c_longlong)]
 
 
+class ScanPointC(C.Structure):
+    """cisdc_scan_point == cisdc::ScanPoint (analysis.hpp:79-87)."""
+    _fields_ = [("scheme", C.c_int), ("M", C.c_int), ("nu", C.c_int), ("a", C.c_double), ("d", C.c_double),
+                ("r", C.c_double), ("dt", C.c_double), ("gamma", C.c_double), ("ok", C.c_int)]
+
+
+_ip = C.POINTER(C.c_int)
+
 GPU_SYMBOLS = [
     ("cisdc_make_quadrature_tables", C.c_int, [C.c_int, C.c_int, C.POINTER(TablesC)]),
     ("cisdc_gpu_create", C.c_int, [C.POINTER(ProblemDescC), C.POINTER(TablesC), C.POINTER(_vp)]),
@@ -129,6 +137,12 @@ GPU_SYMBOLS = [
     ("cisdc_gpu_launch_count", C.c_longlong, [_vp]),
     ("cisdc_gpu_newton_residual_exits", C.c_longlong, [_vp]),
     ("cisdc_gpu_fp64_peak", C.c_int, [_dp, _dp]),
+    ("cisdc_gpu_spectral_radius_scan", C.c_int, [_ip, C.c_int, _ip, C.c_int, _dp, C.c_int, C.c_int, C.c_double,
+                                                 C.c_double, C.c_double, C.c_int, C.c_int, C.POINTER(ScanPointC),
+                                                 C.c_size_t, C.POINTER(C.c_size_t), _dp]),
+    ("cisdc_log_r_grid", C.c_int, [C.c_double, C.c_double, C.c_int, _dp, C.c_size_t]),
+    ("cisdc_gpu_spectral_radius_batch", C.c_int, [_dp, C.c_int, C.c_int, _dp, _ip]),
+    ("cisdc_last_error", C.c_char_p, []),
     ("cisdc_rtc_compile_check", C.c_int, [C.POINTER(ProblemDescC), C.c_char_p, C.c_size_t]),
     ("cisdc_gpu_set_trace", C.c_int, [_vp, C.c_int]),
     ("cisdc_gpu_last_trace", C.c_int, [_vp, C.POINTER(CellTraceC), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

@@ -512,3 +512,85 @@ def integrate(problem_desc, phi0: np.ndarray, opt: IntegrateOptions, ctx: Option
     finally:
         if own:
             ctx.close()
+
+
+# ----------------------------------------------------------------------------- iteration-matrix scans
+
+@dataclass
+class ScanOptions:
+    """cisdc::ScanOptions (analysis.hpp:63-76)."""
+    schemes: list
+    nu_list: list = None
+    r_grid: list = None
+    d_rule: int = 0          # DRule::half_of_r (d = r / 2); 1 = fixed
+    fixed_d: float = -5.0
+    a: float = 1.0
+    dt: float = 1.0
+    M: int = 4
+    convention: int = EulerConvention.literal
+
+
+@dataclass
+class ScanPoint:
+    scheme: int
+    M: int
+    nu: int
+    a: float
+    d: float
+    r: float
+    dt: float
+    gamma: float
+    ok: bool
+
+
+def log_r_grid(lo_exp: float = -2.0, hi_exp: float = 6.0, points_per_decade: int = 40) -> np.ndarray:
+    """cisdc::log_r_grid (analysis.cpp:255-266), evaluated by the library (same std::pow)."""
+    lib = _abi.load()
+    n = lib.cisdc_log_r_grid(lo_exp, hi_exp, points_per_decade, None, 0)
+    if n < 0:
+        raise ValueError(lib.cisdc_last_error().decode())
+    out = np.empty(n)
+    lib.cisdc_log_r_grid(lo_exp, hi_exp, points_per_decade, _abi.dptr(out), n)
+    return out
+
+
+def spectral_radius_scan(opt: ScanOptions, return_matrices: bool = False):
+    """cisdc::spectral_radius_scan (analysis.cpp:270-293) on the GPU: one thread per (scheme, nu, r)
+    point builds the affine iteration matrix of one sweep on the linear model and its spectral
+    radius.  Returns the points (and the M x M matrices G when asked)."""
+    lib = _abi.load()
+    sch = np.ascontiguousarray(opt.schemes, dtype=np.int32)
+    nus = np.ascontiguousarray(opt.nu_list or [], dtype=np.int32)
+    rg = np.ascontiguousarray(opt.r_grid if opt.r_grid is not None else [], dtype=np.float64)
+    groups = sum(len(nus) if s == Scheme.cisdcq else 1 for s in sch)
+    cap = max(groups * len(rg), 1)
+    out = (_abi.ScanPointC * cap)()
+    n = C.c_size_t()
+    G = np.zeros(cap * opt.M * opt.M) if return_matrices else None
+    ip = C.POINTER(C.c_int)
+    rc = lib.cisdc_gpu_spectral_radius_scan(sch.ctypes.data_as(ip), len(sch),
+                                            nus.ctypes.data_as(ip) if len(nus) else None, len(nus),
+                                            _abi.dptr(rg) if len(rg) else None, len(rg), int(opt.d_rule),
+                                            float(opt.fixed_d), float(opt.a), float(opt.dt), int(opt.M),
+                                            int(opt.convention), out, cap, C.byref(n),
+                                            _abi.dptr(G) if return_matrices else None)
+    raise_for(rc, lib.cisdc_last_error().decode())
+    pts = [ScanPoint(p.scheme, p.M, p.nu, p.a, p.d, p.r, p.dt, p.gamma, bool(p.ok)) for p in out[: n.value]]
+    if return_matrices:
+        return pts, G[: n.value * opt.M * opt.M].reshape(n.value, opt.M, opt.M)
+    return pts
+
+
+def spectral_radius_batch(A: np.ndarray):
+    """cisdc::spectral_radius (linalg.cpp:197-332) of a batch of n x n matrices (n <= 8), one GPU thread
+    each.  Returns (rho, status): status 0 ok, 1 non-finite entry, 2 QR iteration cap."""
+    lib = _abi.load()
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    if A.ndim == 2:
+        A = A[None]
+    count, n = A.shape[0], A.shape[1]
+    rho = np.zeros(count)
+    st = np.zeros(count, dtype=np.int32)
+    rc = lib.cisdc_gpu_spectral_radius_batch(_abi.dptr(A), n, count, _abi.dptr(rho), st.ctypes.data_as(C.POINTER(C.c_int)))
+    raise_for(rc, lib.cisdc_last_error().decode())
+    return rho, st

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/cisdc_gpu.h"
+#include "analysis.cuh"
 #include "circulant.hpp"
 #include "common.cuh"
 #include "multigrid.cuh"
@@ -535,7 +536,11 @@ int linear_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rhs, 
   return CISDC_OK;
 }
 
-int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* out, cudaStream_t s) {
+// ev (optional): F_A/F_D of the result wanted right after the solve; *ev_done reports whether the
+// multigrid solve produced them (fused into its last check), else the caller evaluates
+int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* out, cudaStream_t s,
+                    const MgEvalRequest* ev = nullptr, bool* ev_done = nullptr) {
+  if (ev_done) *ev_done = false;
   const long long n = ctx->g.n;
   if (ctx->linear) return linear_solve(ctx, CISDC_STAGE_DIFFUSION, coef, rhs, out, s);
   if (ctx->ref_rd) {
@@ -560,7 +565,7 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
   }
   if (ctx->desc.diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
     const int rc = mg_solve(ctx->mg, ctx->g, ctx->desc, coef, rhs, out, ctx->d_st,
-                            next_tag(ctx, CISDC_STAGE_DIFFUSION), s, &ctx->tm);
+                            next_tag(ctx, CISDC_STAGE_DIFFUSION), s, &ctx->tm, ev, ev_done);
     if (rc) return set_err(ctx, rc, "multigrid launch failed");
     return CISDC_OK;
   }
@@ -921,11 +926,15 @@ int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt
   const double coef = dt * QI(ctx->tb, row, m - 1);
   if (!rhs_ready) TRY(launch_rhs(ctx, diffusion_rhs(ctx, W, m, ell, dt), s));
   double* out = W.get(0, m, ell);
-  TRY(solve_diffusion(ctx, coef, ctx->rhs_d, out, s));
-  if (c) ++c->diffusion;
   // fa_ad / fd_ad of slot (m, 1) are read only by D(m+1, 1) (integrators.cpp:215-216): the
-  // reference's evaluation at m = M has no reader and is skipped
-  if (ell == 1 && m < ctx->M) TRY(launch_eval_ad(ctx, out, ctx->fa_ad[m], ctx->fd_ad[m], s));
+  // reference's evaluation at m = M has no reader and is skipped.  A multigrid solve may produce
+  // them in its last check (k_mg3_check_eval); otherwise they are evaluated here.
+  const bool want = ell == 1 && m < ctx->M;
+  const MgEvalRequest ev{ctx->fa_ad[m], ctx->fd_ad[m], &ctx->ops, &ctx->g};
+  bool done = false;
+  TRY(solve_diffusion(ctx, coef, ctx->rhs_d, out, s, want ? &ev : nullptr, &done));
+  if (c) ++c->diffusion;
+  if (want && !done) TRY(launch_eval_ad(ctx, out, ctx->fa_ad[m], ctx->fd_ad[m], s));
   return CISDC_OK;
 }
 
@@ -1589,6 +1598,169 @@ int cisdc_rtc_compile_check(const cisdc_problem_desc* d, char* log, size_t cap) 
   const int rc = rtc_build(r, rx, d->nspecies, d->ndim, false);
   if (log && cap) std::snprintf(log, cap, "%s", (rc ? r.log : std::string("ok\n") + r.log).c_str());
   return rc;
+}
+
+// ---------------------------------------------------------------- iteration-matrix scans
+
+static thread_local std::string g_last_err;
+const char* cisdc_last_error(void) { return g_last_err.c_str(); }
+
+int cisdc_log_r_grid(double lo_exp, double hi_exp, int points_per_decade, double* out, size_t cap) {
+  if (points_per_decade < 1) {
+    g_last_err = "log_r_grid: points_per_decade >= 1";
+    return -1;
+  }
+  const int n = static_cast<int>(std::lround((hi_exp - lo_exp) * points_per_decade));
+  for (int i = 0; i <= n; ++i) {
+    const double e = lo_exp + (hi_exp - lo_exp) * i / n;
+    if (out && (size_t)i < cap) out[i] = -std::pow(10.0, e);
+  }
+  return n + 1;
+}
+
+int cisdc_gpu_spectral_radius_scan(const int* schemes, int n_schemes, const int* nu_list, int n_nu,
+                                   const double* r_grid, int n_r, int d_rule, double fixed_d, double a, double dt,
+                                   int M, int convention, cisdc_scan_point* out, size_t cap, size_t* n_out,
+                                   double* G_out) {
+  if (!r_grid || n_r < 1) {
+    g_last_err = "spectral_radius_scan: empty r grid";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  if (!schemes || n_schemes < 1) {
+    g_last_err = "spectral_radius_scan: no schemes";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  if (M < 1 || M > kMaxM) {
+    g_last_err = "spectral_radius_scan: M must be in 1..8";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  ScanArgs A{};
+  std::vector<std::pair<int, int>> groups;
+  for (int i = 0; i < n_schemes; ++i) {
+    if (schemes[i] < 0 || schemes[i] > 3) {
+      g_last_err = "spectral_radius_scan: unknown scheme";
+      return CISDC_E_INVALID_ARGUMENT;
+    }
+    if (schemes[i] == CISDC_SCHEME_CISDCQ) {
+      for (int k = 0; k < n_nu; ++k) groups.push_back({schemes[i], nu_list[k]});
+    } else {
+      groups.push_back({schemes[i], 1});
+    }
+  }
+  if (groups.size() > 64) {
+    g_last_err = "spectral_radius_scan: at most 64 (scheme, nu) groups per call";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  const size_t np = groups.size() * (size_t)n_r;
+  if (n_out) *n_out = np;
+  if (!out || cap < np) {
+    g_last_err = "spectral_radius_scan: output capacity";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  cisdc_tables t;
+  if (make_tables(M, convention, &t)) {
+    g_last_err = "spectral_radius_scan: quadrature tables";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  ScanTables tb{};
+  tb.M = M;
+  for (int m = 0; m < M; ++m) {
+    tb.dtau[m] = t.dtau[m];
+    for (int j = 0; j <= M; ++j) {
+      tb.Q[m][j] = t.Q[m * (M + 1) + j];
+      tb.S[m][j] = t.S[m * (M + 1) + j];
+    }
+    for (int j = 0; j < M; ++j) {
+      tb.QtI[m][j] = t.QtI[m * M + j];
+      tb.QtE[m][j] = t.QtE[m * M + j];
+    }
+  }
+  A.n_points = (int)np;
+  A.n_r = n_r;
+  A.n_groups = (int)groups.size();
+  for (size_t g = 0; g < groups.size(); ++g) {
+    A.scheme[g] = groups[g].first;
+    A.nu[g] = groups[g].second;
+  }
+  A.d_rule = d_rule;
+  A.fixed_d = fixed_d;
+  A.a = a;
+  A.dt = dt;
+  double *d_r = nullptr, *d_gamma = nullptr, *d_G = nullptr;
+  int* d_ok = nullptr;
+  auto fail = [&](cudaError_t e) {
+    cudaFree(d_r);
+    cudaFree(d_gamma);
+    cudaFree(d_ok);
+    cudaFree(d_G);
+    g_last_err = std::string("CUDA error: ") + cudaGetErrorString(e);
+    return CISDC_E_CUDA;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&d_r, sizeof(double) * n_r)) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&d_gamma, sizeof(double) * np)) != cudaSuccess) return fail(e);
+  if ((e = cudaMalloc(&d_ok, sizeof(int) * np)) != cudaSuccess) return fail(e);
+  if (G_out && (e = cudaMalloc(&d_G, sizeof(double) * np * M * M)) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpy(d_r, r_grid, sizeof(double) * n_r, cudaMemcpyHostToDevice)) != cudaSuccess) return fail(e);
+  A.r_grid = d_r;
+  A.gamma = d_gamma;
+  A.ok = d_ok;
+  A.G = d_G;
+  k_spectral_scan<<<(unsigned)((np + 63) / 64), 64>>>(tb, A);
+  if ((e = cudaGetLastError()) != cudaSuccess) return fail(e);
+  std::vector<double> gam(np);
+  std::vector<int> ok(np);
+  if ((e = cudaMemcpy(gam.data(), d_gamma, sizeof(double) * np, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e);
+  if ((e = cudaMemcpy(ok.data(), d_ok, sizeof(int) * np, cudaMemcpyDeviceToHost)) != cudaSuccess) return fail(e);
+  if (G_out && (e = cudaMemcpy(G_out, d_G, sizeof(double) * np * M * M, cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return fail(e);
+  for (size_t p = 0; p < np; ++p) {
+    const int g = (int)(p / n_r);
+    const double r = r_grid[p % n_r];
+    cisdc_scan_point& o = out[p];
+    o.scheme = groups[g].first;
+    o.M = M;
+    o.nu = groups[g].second;
+    o.a = a;
+    o.d = d_rule == 0 ? r / 2.0 : fixed_d;
+    o.r = r;
+    o.dt = dt;
+    o.gamma = gam[p];
+    o.ok = ok[p];
+  }
+  cudaFree(d_r);
+  cudaFree(d_gamma);
+  cudaFree(d_ok);
+  cudaFree(d_G);
+  return CISDC_OK;
+}
+
+int cisdc_gpu_spectral_radius_batch(const double* A, int n, int count, double* rho, int* status) {
+  if (n < 1 || n > kMaxM || count < 0 || (count > 0 && (!A || !rho || !status))) {
+    g_last_err = "spectral_radius_batch: n must be in 1..8";
+    return CISDC_E_INVALID_ARGUMENT;
+  }
+  if (count == 0) return CISDC_OK;
+  double *dA = nullptr, *dr = nullptr;
+  int* ds = nullptr;
+  cudaError_t e = cudaMalloc(&dA, sizeof(double) * (size_t)count * n * n);
+  if (e == cudaSuccess) e = cudaMalloc(&dr, sizeof(double) * count);
+  if (e == cudaSuccess) e = cudaMalloc(&ds, sizeof(int) * count);
+  if (e == cudaSuccess) e = cudaMemcpy(dA, A, sizeof(double) * (size_t)count * n * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_spectral_batch<<<(unsigned)((count + 63) / 64), 64>>>(dA, n, count, dr, ds);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(rho, dr, sizeof(double) * count, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(status, ds, sizeof(int) * count, cudaMemcpyDeviceToHost);
+  cudaFree(dA);
+  cudaFree(dr);
+  cudaFree(ds);
+  if (e != cudaSuccess) {
+    g_last_err = std::string("CUDA error: ") + cudaGetErrorString(e);
+    return CISDC_E_CUDA;
+  }
+  return CISDC_OK;
 }
 
 const char* cisdc_gpu_kernel_class_name(int cls) {

@@ -415,6 +415,90 @@ __device__ __forceinline__ void walk_pair(const double* __restrict__ f, const do
   cp_async_wait<0>();
 }
 
+// Per-thread advection state of the pair kernels: face-velocity factors per cell c of the pair
+// (face_u order: (T0 T1) T2; for a = 0 the left face of cell 1 is the right face of cell 0, same
+// product), the z-face carry, and the F_A of a pair from its taps.  Shared by k_eval_ad3_pair and the
+// multigrid check + evaluation kernel (multigrid.cuh), so both compute F_A with the same operations.
+template <bool UCONST>
+struct AdvPair {
+  double pr[2][3], pl[2][3];
+  const double* t2[3];
+  bool adv[3];
+  double ca[3];
+  double t2r[3], t2l[3];
+  double fz_carry[2];
+  int carry_k;
+  __device__ __forceinline__ void init(const Ops& o, const Geom& g) {
+    const int ic = min(blockIdx.x * kPTX + 2 * threadIdx.x, g.nx - 2);
+    const int jc = min(blockIdx.y * kTY + threadIdx.y, g.ny - 1);
+    fz_carry[0] = fz_carry[1] = 0.0;
+    carry_k = -1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      adv[a] = o.adv[a] != 0;
+      ca[a] = o.cadv[a];
+      t2[a] = o.vel[a][2];
+      if (UCONST) continue;
+      const double* t0 = o.vel[a][0];
+      const double* t1 = o.vel[a][1];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int icc = ic + c;
+        const int il = a == 0 ? wrapi(icc - 1, g.nx) : icc, jl = a == 1 ? wrapi(jc - 1, g.ny) : jc;
+        pr[c][a] = (t0 ? __ldg(t0 + icc) : 1.0) * (t1 ? __ldg(t1 + jc) : 1.0);
+        pl[c][a] = (t0 ? __ldg(t0 + il) : 1.0) * (t1 ? __ldg(t1 + jl) : 1.0);
+      }
+    }
+  }
+  __device__ __forceinline__ void plane(const Geom& g, int k) {
+    if (UCONST) return;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      t2r[a] = t2[a] ? __ldg(t2[a] + k) : 1.0;
+      t2l[a] = t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0;
+    }
+  }
+  // acc = -F_A of the pair at plane k (per-cell 5-tap views: x taps of cell c are v.x[c .. c+4])
+  __device__ __forceinline__ void acc(const Ops& o, int k, const PairTaps& v, double (&acc)[2]) {
+    acc[0] = 0.0;
+    acc[1] = 0.0;
+    // axis 0: faces i-1/2, i+1/2, i+3/2
+    if (adv[0]) {
+      const double u_l0 = UCONST ? o.ucon[0] : pl[0][0] * t2l[0];
+      const double u_m = UCONST ? o.ucon[0] : pr[0][0] * t2r[0];
+      const double u_r1 = UCONST ? o.ucon[0] : pr[1][0] * t2r[0];
+      const double f_l0 = u_l0 * (7.0 * (v.x[1] + v.x[2]) - (v.x[0] + v.x[3]));
+      const double f_m = u_m * (7.0 * (v.x[2] + v.x[3]) - (v.x[1] + v.x[4]));
+      const double f_r1 = u_r1 * (7.0 * (v.x[3] + v.x[4]) - (v.x[2] + v.x[5]));
+      acc[0] = acc[0] + (f_m - f_l0) * ca[0];
+      acc[1] = acc[1] + (f_r1 - f_m) * ca[0];
+    }
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      if (adv[1]) {
+        const double ur = UCONST ? o.ucon[1] : pr[c][1] * t2r[1];
+        const double ul = UCONST ? o.ucon[1] : pl[c][1] * t2l[1];
+        const double fr = ur * (7.0 * (v.y[c][2] + v.y[c][3]) - (v.y[c][1] + v.y[c][4]));
+        const double fl = ul * (7.0 * (v.y[c][1] + v.y[c][2]) - (v.y[c][0] + v.y[c][3]));
+        acc[c] = acc[c] + (fr - fl) * ca[1];
+      }
+      if (adv[2]) {
+        const double ur = UCONST ? o.ucon[2] : pr[c][2] * t2r[2];
+        const double fr = ur * (7.0 * (v.z[c][2] + v.z[c][3]) - (v.z[c][1] + v.z[c][4]));
+        double fl;
+        if (carry_k == k) {
+          fl = fz_carry[c];
+        } else {
+          const double ul = UCONST ? o.ucon[2] : pl[c][2] * t2l[2];
+          fl = ul * (7.0 * (v.z[c][1] + v.z[c][2]) - (v.z[c][0] + v.z[c][3]));
+        }
+        fz_carry[c] = fr;
+        acc[c] = acc[c] + (fr - fl) * ca[2];
+      }
+    }
+  }
+};
+
 // F_A and/or F_D, 3-D periodic, two cells per thread (nx even); UCONST as k_eval_ad3_tiled.
 template <bool UCONST>
 __global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_pair(Ops o, Geom g, const double* __restrict__ phi,
@@ -425,82 +509,17 @@ __global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_pair(Ops 
   double* fas = fa ? opaque(fa + sbase) : nullptr;
   double* fds = fd ? opaque(fd + sbase) : nullptr;
   const int s = z.s;
-  const int ic = min(blockIdx.x * kPTX + 2 * threadIdx.x, g.nx - 2);
-  const int jc = min(blockIdx.y * kTY + threadIdx.y, g.ny - 1);
-  // face-velocity factors per cell c of the pair (face_u order: (T0 T1) T2); for a = 0 the left
-  // face of cell 1 is the right face of cell 0 (same product)
-  double pr[2][3], pl[2][3];
-  const double* t2[3];
-  bool adv[3];
-  double cd[3], ca[3];
+  double cd[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    adv[a] = o.adv[a] != 0;
-    cd[a] = o.cdiff[s][a];
-    ca[a] = o.cadv[a];
-    t2[a] = o.vel[a][2];
-    if (UCONST) continue;
-    const double* t0 = o.vel[a][0];
-    const double* t1 = o.vel[a][1];
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int icc = ic + c;
-      const int il = a == 0 ? wrapi(icc - 1, g.nx) : icc, jl = a == 1 ? wrapi(jc - 1, g.ny) : jc;
-      pr[c][a] = (t0 ? __ldg(t0 + icc) : 1.0) * (t1 ? __ldg(t1 + jc) : 1.0);
-      pl[c][a] = (t0 ? __ldg(t0 + il) : 1.0) * (t1 ? __ldg(t1 + jl) : 1.0);
-    }
-  }
-  double t2r[3], t2l[3];
-  double fz_carry[2] = {0.0, 0.0};
-  int carry_k = -1;
+  for (int a = 0; a < 3; ++a) cd[a] = o.cdiff[s][a];
+  AdvPair<UCONST> ad;
+  ad.init(o, g);
   walk_pair<false, kRing, 5>(
-      phi + sbase, nullptr, g.nx, g.ny, g.nz, z, pring, nullptr,
-      [&](int k) {
-        if (UCONST) return;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          t2r[a] = t2[a] ? __ldg(t2[a] + k) : 1.0;
-          t2l[a] = t2[a] ? __ldg(t2[a] + (a == 2 ? wrapi(k - 1, g.nz) : k)) : 1.0;
-        }
-      },
+      phi + sbase, nullptr, g.nx, g.ny, g.nz, z, pring, nullptr, [&](int k) { ad.plane(g, k); },
       [&](int k, unsigned cell, const PairTaps& v, const double (&)[2], bool ok) {
-        // per-cell 5-tap views: x taps of cell c are v.x[c .. c+4]
         if (fas) {
-          double acc[2] = {0.0, 0.0};
-          // axis 0: faces i-1/2, i+1/2, i+3/2
-          if (adv[0]) {
-            const double u_l0 = UCONST ? o.ucon[0] : pl[0][0] * t2l[0];
-            const double u_m = UCONST ? o.ucon[0] : pr[0][0] * t2r[0];
-            const double u_r1 = UCONST ? o.ucon[0] : pr[1][0] * t2r[0];
-            const double f_l0 = u_l0 * (7.0 * (v.x[1] + v.x[2]) - (v.x[0] + v.x[3]));
-            const double f_m = u_m * (7.0 * (v.x[2] + v.x[3]) - (v.x[1] + v.x[4]));
-            const double f_r1 = u_r1 * (7.0 * (v.x[3] + v.x[4]) - (v.x[2] + v.x[5]));
-            acc[0] = acc[0] + (f_m - f_l0) * ca[0];
-            acc[1] = acc[1] + (f_r1 - f_m) * ca[0];
-          }
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            if (adv[1]) {
-              const double ur = UCONST ? o.ucon[1] : pr[c][1] * t2r[1];
-              const double ul = UCONST ? o.ucon[1] : pl[c][1] * t2l[1];
-              const double fr = ur * (7.0 * (v.y[c][2] + v.y[c][3]) - (v.y[c][1] + v.y[c][4]));
-              const double fl = ul * (7.0 * (v.y[c][1] + v.y[c][2]) - (v.y[c][0] + v.y[c][3]));
-              acc[c] = acc[c] + (fr - fl) * ca[1];
-            }
-            if (adv[2]) {
-              const double ur = UCONST ? o.ucon[2] : pr[c][2] * t2r[2];
-              const double fr = ur * (7.0 * (v.z[c][2] + v.z[c][3]) - (v.z[c][1] + v.z[c][4]));
-              double fl;
-              if (carry_k == k) {
-                fl = fz_carry[c];
-              } else {
-                const double ul = UCONST ? o.ucon[2] : pl[c][2] * t2l[2];
-                fl = ul * (7.0 * (v.z[c][1] + v.z[c][2]) - (v.z[c][0] + v.z[c][3]));
-              }
-              fz_carry[c] = fr;
-              acc[c] = acc[c] + (fr - fl) * ca[2];
-            }
-          }
+          double acc[2];
+          ad.acc(o, k, v, acc);
           if (ok) {
             __stcg(reinterpret_cast<double2*>(fas + cell), make_double2(-acc[0], -acc[1]));
             flag_wild(o.wild, wild_bits(acc[0]) | wild_bits(acc[1]));
@@ -517,7 +536,7 @@ __global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_pair(Ops 
           }
           if (ok) __stcg(reinterpret_cast<double2*>(fds + cell), make_double2(lap[0], lap[1]));
         }
-        carry_k = k + 1;
+        ad.carry_k = k + 1;
       });
 }
 

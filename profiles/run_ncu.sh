@@ -24,7 +24,7 @@ if [ "${4:-hot}" = "all" ]; then
   # every kernel class of a (small) config: the first ${5:-60} launches, one capture
   cap all ".*" ${5:-60}
 else
-  cap mg3 "k_mg3_tiled|k_mg3_pair" 4
+  cap mg3 "k_mg3_tiled|k_mg3_pair|k_mg3_tma" 4
   cap eval k_eval_ad3 2
   cap react "^k_react$" 2
   cap rhs "^k_rhs$" 2

@@ -553,3 +553,36 @@ def test_device_looped_multigrid_cap(gpu, oracle, cap, monkeypatch):
     loop; the error text equals the oracle's, a run within the cap is bitwise equal."""
     monkeypatch.setenv("CISDC_MG_LOOP", "1")
     test_multigrid_cycle_cap_matches_oracle(gpu, oracle, cap)
+
+
+@pytest.mark.parametrize("n", [(64, 24, 33), (128, 16, 40), (64, 8, 9)])
+def test_tma_staged_multigrid_sweeps(gpu, oracle, n, monkeypatch):
+    """Whole-tile 3-D grids (nx % 64 == 0, ny % 8 == 0) run the level-0 multigrid sweeps and checks on
+    the TMA walker (tma.cuh: five bulk-tensor boxes per plane, mbarrier completion); the cp.async walker
+    is forced with CISDC_MG_TMA=0.  Both bitwise equal to the oracle (and so to each other)."""
+    spec = c5_like(n, P.constant_velocity_tables((1.0, -0.5, 0.25), n))
+    runs = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("CISDC_MG_TMA", flag)
+        _, g, c = per_step_compare(oracle, spec, 2, 1, workers=2)
+        assert np.array_equal(g, c)
+        runs.append(g)
+    assert np.array_equal(runs[0], runs[1])
+
+
+@pytest.mark.parametrize("n,variable", [((64, 24, 33), False), ((40, 20, 36), True), ((37, 12, 40), False)])
+def test_check_eval_fusion_bitwise(gpu, oracle, n, variable, monkeypatch):
+    """CISDCQ's F_A/F_D(phi_AD) produced by the multigrid solve's predicted last check
+    (k_mg3_check_eval: F_D shares the residual's Laplacian, F_A is the evaluation kernel's code) and,
+    with CISDC_MG_CHECK_EVAL=0, by the separate evaluation: both bitwise equal to the oracle (serial
+    and concurrent PMISDC), on tile-aligned, ragged and odd-nx grids (odd nx keeps the separate path)."""
+    vel = random_velocity_tables(n) if variable else P.constant_velocity_tables((1.0, -0.5, 0.25), n)
+    spec = c5_like(n, vel)
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("CISDC_MG_CHECK_EVAL", flag)
+        for workers in (0, 2):
+            _, g, c = per_step_compare(oracle, spec, 2, 2, workers=workers)
+            assert np.array_equal(g, c)
+            out.append(g)
+    assert all(np.array_equal(out[0], x) for x in out[1:])
