@@ -335,7 +335,9 @@ def main():
     dom = max(classes, key=lambda x: x["ms"])
     cell_solves = desc.ncell * spec.M * spec.n_sweeps * args.steps * (spec.nu if scheme == 2 else 1)
     sparse = os.environ.get("CISDC_RTC", "1") != "0"  # the specialised kernel runs the static-pattern LU
-    newton_flops = roofline.newton_work(desc, newton, newton - newton_rexits, sparse=sparse)
+    # the reaction kernel's algorithmic work: the Newton trips and the F_R evaluation of every result
+    newton_flops = roofline.newton_work(desc, newton, newton - newton_rexits, sparse=sparse,
+                                        cell_solves=cell_solves)
     if dom["kernel"] == "react_newton" and desc.nspecies >= 9:
         achieved = newton_flops / (dom["ms"] * 1e-3) / 1e12
         # The kernel's arithmetic is the reference's no-FMA operation sequence (bit parity), i.e.

@@ -172,6 +172,22 @@ struct cisdc_gpu_ctx {
   std::vector<std::pair<int, int>> tags;
   int cur_sweep = 0;   // 1-based sweep of the integrate step being enqueued, 0 outside integrate
   int fail_sweep = 0;  // sweep of the failure the last check_status decoded
+  // Whole integrate steps captured as CUDA graphs (steps without host decisions inside: no stop
+  // tolerance, no host-synchronised multigrid, no live timing or tracing).  A replay stands for the
+  // host enqueue of initialize + n sweeps + the node-0 copy; the host bookkeeping the enqueue did
+  // (tags, stage counts, views, cur) is restored from the capture.
+  struct StepGraph {
+    int scheme, nu, workers, n_sweeps, convention;
+    double dt;
+    cudaGraphExec_t exec;
+    long long kernels;
+    std::vector<std::pair<int, int>> tags;
+    cisdc_counters counts;
+    int cur;
+    const double* view[2][4][kMaxM + 1];
+  };
+  std::vector<StepGraph> step_graphs;
+  long long steps_direct = 0;  // steps enqueued directly (the first one is never captured)
 };
 
 namespace {
@@ -536,11 +552,7 @@ int linear_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rhs, 
   return CISDC_OK;
 }
 
-// ev (optional): F_A/F_D of the result wanted right after the solve; *ev_done reports whether the
-// multigrid solve produced them (fused into its last check), else the caller evaluates
-int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* out, cudaStream_t s,
-                    const MgEvalRequest* ev = nullptr, bool* ev_done = nullptr) {
-  if (ev_done) *ev_done = false;
+int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* out, cudaStream_t s) {
   const long long n = ctx->g.n;
   if (ctx->linear) return linear_solve(ctx, CISDC_STAGE_DIFFUSION, coef, rhs, out, s);
   if (ctx->ref_rd) {
@@ -565,7 +577,7 @@ int solve_diffusion(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* 
   }
   if (ctx->desc.diffusion_solver == CISDC_DIFFUSION_MULTIGRID) {
     const int rc = mg_solve(ctx->mg, ctx->g, ctx->desc, coef, rhs, out, ctx->d_st,
-                            next_tag(ctx, CISDC_STAGE_DIFFUSION), s, &ctx->tm, ev, ev_done);
+                            next_tag(ctx, CISDC_STAGE_DIFFUSION), s, &ctx->tm);
     if (rc) return set_err(ctx, rc, "multigrid launch failed");
     return CISDC_OK;
   }
@@ -926,15 +938,11 @@ int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt
   const double coef = dt * QI(ctx->tb, row, m - 1);
   if (!rhs_ready) TRY(launch_rhs(ctx, diffusion_rhs(ctx, W, m, ell, dt), s));
   double* out = W.get(0, m, ell);
-  // fa_ad / fd_ad of slot (m, 1) are read only by D(m+1, 1) (integrators.cpp:215-216): the
-  // reference's evaluation at m = M has no reader and is skipped.  A multigrid solve may produce
-  // them in its last check (k_mg3_check_eval); otherwise they are evaluated here.
-  const bool want = ell == 1 && m < ctx->M;
-  const MgEvalRequest ev{ctx->fa_ad[m], ctx->fd_ad[m], &ctx->ops, &ctx->g};
-  bool done = false;
-  TRY(solve_diffusion(ctx, coef, ctx->rhs_d, out, s, want ? &ev : nullptr, &done));
+  TRY(solve_diffusion(ctx, coef, ctx->rhs_d, out, s));
   if (c) ++c->diffusion;
-  if (want && !done) TRY(launch_eval_ad(ctx, out, ctx->fa_ad[m], ctx->fd_ad[m], s));
+  // fa_ad / fd_ad of slot (m, 1) are read only by D(m+1, 1) (integrators.cpp:215-216): the
+  // reference's evaluation at m = M has no reader and is skipped
+  if (ell == 1 && m < ctx->M) TRY(launch_eval_ad(ctx, out, ctx->fa_ad[m], ctx->fd_ad[m], s));
   return CISDC_OK;
 }
 
@@ -1121,6 +1129,7 @@ long long cisdc_gpu_newton_residual_exits(const cisdc_gpu_ctx* ctx) {
 void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
   if (!ctx) return;
   cudaDeviceSynchronize();
+  for (auto& g : ctx->step_graphs) cudaGraphExecDestroy(g.exec);
   for (void* p : ctx->allocs) cudaFree(p);
   mg_free(ctx->mg);
   rtc_free(ctx->rtc);
@@ -1481,6 +1490,81 @@ int cisdc_gpu_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rh
 // cisdc::integrate (integrators.cpp:301-333).  Sweeps are enqueued asynchronously; without a
 // stop tolerance the host synchronises once per step (increments and counters are harvested
 // from device memory), with one it must look at every increment.
+// one step's enqueue without host decisions: initialize, n sweeps, node 0 <- phi[M]
+static int enqueue_step(cisdc_gpu_ctx* ctx, const cisdc_integrate_options* o, cisdc_counters* counters, int& done) {
+  TRY(do_initialize(ctx));
+  for (int k = 1; k <= o->n_sweeps; ++k) {
+    ctx->cur_sweep = k;
+    done = k - 1;
+    TRY(run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, counters, k - 1));
+  }
+  CU(cudaMemcpyAsync(ctx->node0[kPhi], V(ctx, ctx->cur, kPhi, ctx->M), sizeof(double) * ctx->g.n,
+                     cudaMemcpyDeviceToDevice, ctx->s_main));
+  return CISDC_OK;
+}
+
+// whole-step graphs (CISDC_STEP_GRAPH=0: every step enqueued directly)
+static bool step_graph_ok(const cisdc_gpu_ctx* ctx, const cisdc_integrate_options* o) {
+  const char* e = std::getenv("CISDC_STEP_GRAPH");
+  if (e && e[0] == '0') return false;
+  const bool host_mg = !ctx->ref_rd && !ctx->linear && ctx->desc.diffusion_solver == CISDC_DIFFUSION_MULTIGRID;
+  return !o->has_stop_tol && !ctx->tm.on && !ctx->trace_on && !host_mg;
+}
+
+static cisdc_gpu_ctx::StepGraph* find_step_graph(cisdc_gpu_ctx* ctx, const cisdc_integrate_options* o) {
+  for (auto& g : ctx->step_graphs)
+    if (g.scheme == o->scheme && g.nu == o->nu && g.workers == o->workers && g.n_sweeps == o->n_sweeps &&
+        g.convention == ctx->tb.convention && g.dt == o->dt)
+      return &g;
+  return nullptr;
+}
+
+// capture one step (nothing executes); nullptr when capture is not possible
+static cisdc_gpu_ctx::StepGraph* capture_step_graph(cisdc_gpu_ctx* ctx, const cisdc_integrate_options* o) {
+  cudaStream_t s = ctx->s_main;
+  const long long launches0 = ctx->tm.launches;
+  ctx->tags.clear();
+  cisdc_counters counts{};
+  int done = 0;
+  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return nullptr;
+  const int rc = enqueue_step(ctx, o, &counts, done);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(s, &graph);
+  cudaGetLastError();
+  cisdc_gpu_ctx::StepGraph g{};
+  g.kernels = ctx->tm.launches - launches0;
+  ctx->tm.launches = launches0;
+  if (rc || ec != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    ctx->tags.clear();
+    return nullptr;
+  }
+  const cudaError_t ei = cudaGraphInstantiate(&g.exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ei != cudaSuccess) {
+    cudaGetLastError();
+    ctx->tags.clear();
+    return nullptr;
+  }
+  g.scheme = o->scheme;
+  g.nu = o->nu;
+  g.workers = o->workers;
+  g.n_sweeps = o->n_sweeps;
+  g.convention = ctx->tb.convention;
+  g.dt = o->dt;
+  g.tags = ctx->tags;
+  g.counts = counts;
+  g.cur = ctx->cur;
+  std::memcpy(g.view, ctx->view, sizeof(g.view));
+  ctx->tags.clear();
+  if (ctx->step_graphs.size() >= 8) {
+    cudaGraphExecDestroy(ctx->step_graphs.front().exec);
+    ctx->step_graphs.erase(ctx->step_graphs.begin());
+  }
+  ctx->step_graphs.push_back(g);
+  return &ctx->step_graphs.back();
+}
+
 static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_device, size_t n,
                           const cisdc_integrate_options* o, double* final_state, bool final_device,
                           cisdc_step_report* reports, double* increments) {
@@ -1501,7 +1585,6 @@ static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_devi
   CU(cudaMemcpyAsync(ctx->node0[kPhi], phi0, sizeof(double) * n,
                      phi0_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
   for (int step = 0; step < o->n_steps; ++step) {
-    TRY(do_initialize(ctx));
     cisdc_step_report rep{};
     int done = 0;
     // the reference's context prefix (integrators.cpp:320-321); the sweep comes from the failure's
@@ -1514,6 +1597,7 @@ static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_devi
     };
     ctx->fail_sweep = 0;
     if (o->has_stop_tol) {
+      TRY(do_initialize(ctx));
       for (int k = 1; k <= o->n_sweeps; ++k) {
         ctx->cur_sweep = k;
         int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters, k - 1);
@@ -1525,11 +1609,29 @@ static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_devi
         done = k;
         if (ctx->h_incr[k - 1] <= o->stop_tol) break;
       }
+      // start = state.phi[M] becomes node 0 of the next step
+      CU(cudaMemcpyAsync(ctx->node0[kPhi], V(ctx, ctx->cur, kPhi, ctx->M), sizeof(double) * n,
+                         cudaMemcpyDeviceToDevice, s));
     } else {
-      for (int k = 1; k <= o->n_sweeps; ++k) {
-        ctx->cur_sweep = k;
-        done = k - 1;
-        const int rc = run_one_sweep(ctx, o->scheme, o->dt, o->nu, o->workers, &rep.counters, k - 1);
+      cisdc_gpu_ctx::StepGraph* sg = nullptr;
+      if (step_graph_ok(ctx, o) && ctx->steps_direct > 0) {
+        sg = find_step_graph(ctx, o);
+        if (!sg) sg = capture_step_graph(ctx, o);
+      }
+      if (sg) {  // replay: the captured enqueue, and the host bookkeeping it did
+        CU(cudaGraphLaunch(sg->exec, s));
+        ctx->tm.add_launches(sg->kernels);
+        ctx->tags = sg->tags;
+        rep.counters.diffusion += sg->counts.diffusion;
+        rep.counters.reaction += sg->counts.reaction;
+        rep.counters.coupled += sg->counts.coupled;
+        ctx->cur = sg->cur;
+        std::memcpy(ctx->view, sg->view, sizeof(ctx->view));
+        ctx->have_incr = false;
+        done = o->n_sweeps - 1;
+      } else {
+        const int rc = enqueue_step(ctx, o, &rep.counters, done);
+        ++ctx->steps_direct;
         if (rc) return fail(rc);
       }
       CU(cudaMemcpyAsync(ctx->h_incr, ctx->d_incr, sizeof(double) * o->n_sweeps, cudaMemcpyDeviceToHost, s));
@@ -1544,8 +1646,6 @@ static int integrate_impl(cisdc_gpu_ctx* ctx, const double* phi0, bool phi0_devi
     ctx->have_incr = true;
     rep.sweeps = done;
     if (reports) reports[step] = rep;
-    // start = state.phi[M] becomes node 0 of the next step
-    CU(cudaMemcpyAsync(ctx->node0[kPhi], V(ctx, ctx->cur, kPhi, ctx->M), sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
   }
   CU(cudaMemcpyAsync(final_state, ctx->node0[kPhi], sizeof(double) * n,
                      final_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));

@@ -425,69 +425,6 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_tma(const __grid_constant__
   if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
 }
 
-// A solve's predicted last check fused with the evaluation the sweep needs right after the solve:
-// F_A and F_D at the final iterate (CISDCQ's D(m, 1) cell evaluates F_A/F_D(phi_AD[m]), integrators.cpp
-// :215-216).  The check's residual b - (x - coef lap) and F_D share lap: on level 0 the multigrid
-// coefficients c_sa are ops.cdiff[s][a] (both d_s / (12 h_a^2)) and the 5-tap expression and axis
-// order are the evaluation's, so F_D = lap bit for bit; F_A comes from AdvPair, the evaluation
-// kernel's own code.  Species that met the tolerance at x = b (cycles == 0) evaluate at b, the rest at
-// the level-0 iterate; only active species reduce the residual norm.  One pass reads x and b and
-// writes F_A and F_D instead of a check pass (x, b) plus an evaluation pass (x, F_A, F_D).
-struct CheckEvalArgs {
-  const double* x;
-  const double* b;
-  const int* cycles;
-  const int* active;
-  double* rmax;
-  double* fa;
-  double* fd;
-};
-template <bool UCONST>
-__global__ void __launch_bounds__(kTX* kTY, 2) k_mg3_check_eval(const __grid_constant__ MgCoef C, Ops o, Geom g,
-                                                                CheckEvalArgs A, int kc) {
-  extern __shared__ __align__(16) double mg_cering[];
-  __shared__ double red[kTX * kTY / 32];
-  __shared__ double redb[kTX * kTY / 32];
-  const ZChunk z = zchunk(g.nz, kc);
-  const int s = z.s;
-  const bool act = A.active[s] != 0;  // uniform per block
-  const long long sbase = (long long)s * g.ncell;
-  const double* xs = (A.cycles[s] == 0 ? A.b : A.x) + sbase;
-  double* fas = opaque(A.fa + sbase);
-  double* fds = opaque(A.fd + sbase);
-  const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef;
-  AdvPair<UCONST> ad;
-  ad.init(o, g);
-  double m = 0.0;
-  walk_pair<true, kMgRing, kMgRing - 2>(
-      xs, A.b + sbase, g.nx, g.ny, g.nz, z, mg_cering, mg_cering + kMgRing * kPPlaneSlot,
-      [&](int k) { ad.plane(g, k); },
-      [&](int k, unsigned cell, const PairTaps& v, const double (&bv)[2], bool ok) {
-        double lap[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          double l = 0.0;
-          l = l + cs0 * (-v.x[c] + 16.0 * v.x[c + 1] - 30.0 * v.x[c + 2] + 16.0 * v.x[c + 3] - v.x[c + 4]);
-          l = l + cs1 * (-v.y[c][0] + 16.0 * v.y[c][1] - 30.0 * v.y[c][2] + 16.0 * v.y[c][3] - v.y[c][4]);
-          l = l + cs2 * (-v.z[c][0] + 16.0 * v.z[c][1] - 30.0 * v.z[c][2] + 16.0 * v.z[c][3] - v.z[c][4]);
-          lap[c] = l;
-          if (act) {
-            const double r = bv[c] - (v.x[c + 2] - coef * l);
-            m = max_keep(m, ok ? fabs(r) : 0.0);
-          }
-        }
-        double acc[2];
-        ad.acc(o, k, v, acc);
-        if (ok) {
-          __stcg(reinterpret_cast<double2*>(fas + cell), make_double2(-acc[0], -acc[1]));
-          flag_wild(o.wild, wild_bits(acc[0]) | wild_bits(acc[1]));
-          __stcg(reinterpret_cast<double2*>(fds + cell), make_double2(lap[0], lap[1]));
-        }
-        ad.carry_k = k + 1;
-      });
-  if (act) block_max_atomic<false>(m, 0.0, red, redb, A.rmax + s, nullptr);
-}
-
 // 2-D level sweep / check on the row-streaming walker (stencil2d.cuh; nx even): per cell the
 // expression of k_mg_smooth<2> / mg_ax<2>.  Dynamic shared memory kRowSmem.
 template <bool SMOOTH, bool NORM, bool BMAX>
@@ -1010,24 +947,6 @@ inline bool mg_tma_enabled() {
              cudaSuccess;
 }
 
-// The evaluation a caller wants of the solve's result (F_A and F_D of `out`); mg_solve reports
-// whether it was produced by the last check (k_mg3_check_eval).
-struct MgEvalRequest {
-  double* fa;
-  double* fd;
-  const Ops* ops;
-  const Geom* geom;
-};
-
-// the predicted last check fused with the caller's evaluation (CISDC_MG_CHECK_EVAL=0: separate)
-inline bool mg_check_eval_enabled() {  // read per solve, so a process can switch it (tests do)
-  const char* e = std::getenv("CISDC_MG_CHECK_EVAL");
-  if (!(e && e[0] == '1')) return false;
-  const int sm = (int)kMgPairSmem;
-  return func_attr_once(k_mg3_check_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess &&
-         func_attr_once(k_mg3_check_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm) == cudaSuccess;
-}
-
 // Wraps the engine's hook while a cycle is captured: counts the kernels (the replays are charged
 // that many launches) and forwards nothing else (no timing events inside a graph).
 struct CountingHook final : LaunchHook {
@@ -1083,24 +1002,6 @@ struct MgRunner {
       k_mg_update<<<1, 32, 0, s>>>(h.S, d.mg_tol, d.mg_max_cycles, h.d_active, h.d_cycles, h.d_bmax, h.d_rmax,
                                    h.d_flag, st, h.d_tag, count);
     hook->after(kKMgNorm, s, 0.0);
-  }
-
-  // check_only fused with F_A/F_D of the final iterate (k_mg3_check_eval); false when the grid or
-  // the level does not allow it (the caller then runs check_only and evaluates separately)
-  bool check_only_eval(const MgEvalRequest& ev) {
-    MgLevel& Lv = h.lv[0];
-    if (DIM != 3 || !tile3d_ok(Lv.ncell) || Lv.nx % 2 != 0 || !mg_pair_enabled() || !mg_check_eval_enabled())
-      return false;
-    CheckEvalArgs A{Lv.x, b0, h.d_cycles, h.d_active, h.d_rmax, ev.fa, ev.fd};
-    const dim3 pg = tile3d_pair_grid(Lv.nx, Lv.ny, Lv.nz, h.S);
-    hook->before(kKEvalAD, s);
-    if (ev.ops->vconst)
-      k_mg3_check_eval<true><<<pg, dim3(kTX, kTY), kMgPairSmem, s>>>(C[0], *ev.ops, *ev.geom, A, kZChunk);
-    else
-      k_mg3_check_eval<false><<<pg, dim3(kTX, kTY), kMgPairSmem, s>>>(C[0], *ev.ops, *ev.geom, A, kZChunk);
-    hook->after(kKEvalAD, s, 16.0 * (double)Lv.ncell * h.S);  // F_A, F_D written (x, b: the check's bytes)
-    update(0);
-    return true;
   }
 
   // The predicted last check of a solve without the sweep fused to it: ||b - A x||_inf of the
@@ -1423,9 +1324,7 @@ inline MgHierarchy::SolveGraph* mg_solve_graph(MgHierarchy& h, MgRunner<DIM>& R,
 // separate residual-norm pass.
 template <int DIM>
 inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
-                        double* out, DevStatus* st, unsigned tag, cudaStream_t s, LaunchHook* hook,
-                        const MgEvalRequest* ev = nullptr, bool* ev_done = nullptr) {
-  if (ev_done) *ev_done = false;
+                        double* out, DevStatus* st, unsigned tag, cudaStream_t s, LaunchHook* hook) {
   const long long n = g.n;
   if (coef == 0.0) {
     if (cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s) != cudaSuccess) return CISDC_E_CUDA;
@@ -1489,7 +1388,6 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
     if (pc.first == coef) batch = std::max(1, pc.second);
   int launched = 0;   // V-cycles enqueued
   int chk_only = -1;  // real cycles enqueued before the check-only pass (-1: none)
-  bool ev_fused = false;
   if (fused) {
     // cycle i checks x_{i-1} first: n real cycles need n + 1 enqueued ones.  Cycles after the first
     // replay a captured graph of the cycle (same kernels, same pointers: the sweep counts per level
@@ -1502,10 +1400,8 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
       for (int b = 0; b < batch && launched <= d.mg_max_cycles; ++b, ++launched) {
         if (first_batch && b == batch - 1 && b >= 1 && mg_check_only_enabled()) {
           // the predicted convergence check: residual only (a misprediction costs this pass; the
-          // next cycle's fused check repeats the decision), with the caller's evaluation of the
-          // result when it can be fused (valid only if this check ends the solve)
-          if (ev && R.check_only_eval(*ev)) ev_fused = true;
-          else R.check_only();
+          // next cycle's fused check repeats the decision)
+          R.check_only();
           chk_only = b;
           --launched;  // not a V-cycle: the cap counts real cycles only (the (N+1)-th fused check
                        // must still test x_N and flag the cap)
@@ -1526,8 +1422,6 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
       }
       cudaMemcpyAsync(h.h_flag, h.d_flag, sizeof(int) * 2, cudaMemcpyDeviceToHost, s);
       if (cudaStreamSynchronize(s) != cudaSuccess) return CISDC_E_CUDA;
-      // the fused evaluation saw the final iterate iff its check ended the solve
-      if (first_batch && ev_fused && ev_done && !h.h_flag[0] && !h.h_flag[1]) *ev_done = true;
       if (!h.h_flag[0] || h.h_flag[1] || launched > d.mg_max_cycles) break;
       batch = 1;
       first_batch = false;
@@ -1610,15 +1504,12 @@ inline int mg_solve_dim(MgHierarchy& h, const Geom& g, const cisdc_problem_desc&
   return CISDC_OK;
 }
 
-// ev (optional): F_A/F_D of the solution wanted right after the solve; *ev_done reports whether the
-// solve produced them (fused into its last check), else the caller evaluates.
 inline int mg_solve(MgHierarchy& h, const Geom& g, const cisdc_problem_desc& d, double coef, const double* rhs,
-                    double* out, DevStatus* st, unsigned tag, cudaStream_t s, LaunchHook* hook,
-                    const MgEvalRequest* ev = nullptr, bool* ev_done = nullptr) {
+                    double* out, DevStatus* st, unsigned tag, cudaStream_t s, LaunchHook* hook) {
   switch (g.ndim) {
-    case 1: return mg_solve_dim<1>(h, g, d, coef, rhs, out, st, tag, s, hook, ev, ev_done);
-    case 2: return mg_solve_dim<2>(h, g, d, coef, rhs, out, st, tag, s, hook, ev, ev_done);
-    default: return mg_solve_dim<3>(h, g, d, coef, rhs, out, st, tag, s, hook, ev, ev_done);
+    case 1: return mg_solve_dim<1>(h, g, d, coef, rhs, out, st, tag, s, hook);
+    case 2: return mg_solve_dim<2>(h, g, d, coef, rhs, out, st, tag, s, hook);
+    default: return mg_solve_dim<3>(h, g, d, coef, rhs, out, st, tag, s, hook);
   }
 }
 

@@ -88,9 +88,19 @@ def newton_flops(desc, sparse: bool = True) -> tuple[float, float]:
     return float(residual), float(jac + shift + lu + back + update)
 
 
-def newton_work(desc, trips: int, full_trips: int, sparse: bool = True) -> float:
+def rates_flops(desc) -> float:
+    """FP64 flops of one F_R evaluation at a cell (the rates and the stoichiometric sums), the work
+    the reaction kernel does after the solve for the stage's F_R output (eval_reaction)."""
+    if desc.reaction_kind != _abi.REACTION_MASS_ACTION:
+        return 4.0 if desc.reaction_kind == _abi.REACTION_BISTABLE else 1.0
+    S, reac, nu = _network(desc)
+    return float(sum(2 if reac[r, 1] >= 0 else 1 for r in range(len(reac))) + 2 * int(np.count_nonzero(nu)))
+
+
+def newton_work(desc, trips: int, full_trips: int, sparse: bool = True, cell_solves: int = 0) -> float:
     """Lower-bound FP64 flops of `trips` Newton trips, `full_trips` of which built and solved the
     Jacobian (the others ended at the residual test |f| <= tol; the device counts those exits,
-    cisdc_gpu_newton_residual_exits).  Every trip evaluates the residual."""
+    cisdc_gpu_newton_residual_exits), plus the F_R evaluation at each of `cell_solves` results.
+    Every trip evaluates the residual."""
     res, full = newton_flops(desc, sparse)
-    return trips * res + max(full_trips, 0) * full
+    return trips * res + max(full_trips, 0) * full + cell_solves * rates_flops(desc)

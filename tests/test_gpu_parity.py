@@ -570,19 +570,57 @@ def test_tma_staged_multigrid_sweeps(gpu, oracle, n, monkeypatch):
     assert np.array_equal(runs[0], runs[1])
 
 
-@pytest.mark.parametrize("n,variable", [((64, 24, 33), False), ((40, 20, 36), True), ((37, 12, 40), False)])
-def test_check_eval_fusion_bitwise(gpu, oracle, n, variable, monkeypatch):
-    """CISDCQ's F_A/F_D(phi_AD) produced by the multigrid solve's predicted last check
-    (k_mg3_check_eval: F_D shares the residual's Laplacian, F_A is the evaluation kernel's code) and,
-    with CISDC_MG_CHECK_EVAL=0, by the separate evaluation: both bitwise equal to the oracle (serial
-    and concurrent PMISDC), on tile-aligned, ragged and odd-nx grids (odd nx keeps the separate path)."""
-    vel = random_velocity_tables(n) if variable else P.constant_velocity_tables((1.0, -0.5, 0.25), n)
-    spec = c5_like(n, vel)
-    out = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("CISDC_MG_CHECK_EVAL", flag)
-        for workers in (0, 2):
-            _, g, c = per_step_compare(oracle, spec, 2, 2, workers=workers)
-            assert np.array_equal(g, c)
-            out.append(g)
-    assert all(np.array_equal(out[0], x) for x in out[1:])
+@pytest.mark.parametrize("case", ["c0", "c1", "c2", "linear"])
+def test_step_graph_replay_bitwise(gpu, oracle, case, monkeypatch):
+    """Steps without host decisions inside (no stop tolerance, no host-synchronised multigrid) are
+    captured once as a CUDA graph and replayed (the first step of a context runs directly): the
+    final state, per-step sweeps, stage counts, Newton counts and increments equal both the direct
+    enqueue (CISDC_STEP_GRAPH=0) and the oracle, over several steps and every scheme."""
+    if case == "c0":
+        spec, schemes = P.config_c0(n_steps=4), ((0, 1), (1, 1), (2, 3))
+    elif case == "c1":
+        spec, schemes = P.config_c1(), ((0, 1), (2, 1))
+    elif case == "c2":
+        spec, schemes = P.config_c2(scale=16, n_steps=3), ((1, 1), (2, 1))
+    else:
+        p = P.linear_scalar(0.5, -40.0, -3.0, batch=4097)
+        spec = P.RunSpec(p, np.linspace(-1.0, 1.0, 4097), 3, 3, 4, 0.05, 3, name="linear")
+        schemes = ((3, 1), (2, 2))
+    for scheme, nu in schemes:
+        res = {}
+        for flag in ("1", "0"):
+            monkeypatch.setenv("CISDC_STEP_GRAPH", flag)
+            o = opts(spec, scheme, steps=min(spec.n_steps, 6), nu=nu, workers=2 if scheme == 2 else 0)
+            ctx = api.GpuContext(spec.problem, spec.M, spec.convention)
+            try:
+                api.integrate(spec.problem, spec.phi0, o, ctx=ctx)  # the context's first step runs directly
+                res[flag] = api.integrate(spec.problem, spec.phi0, o, ctx=ctx)
+            finally:
+                ctx.close()
+        c, reps, incs = oracle.integrate(spec.problem, spec.phi0, o)
+        g, d = res["1"], res["0"]
+        assert np.array_equal(g.final_state, d.final_state) and np.array_equal(g.final_state, c)
+        for a, b, r in zip(g.steps, d.steps, reps):
+            assert a.sweeps == b.sweeps == r.sweeps
+            assert (a.counters.diffusion, a.counters.reaction, a.counters.coupled, a.counters.newton_iterations) == \
+                (r.counters.diffusion, r.counters.reaction, r.counters.coupled, r.counters.newton_iterations)
+            assert np.array_equal(a.increments, b.increments)
+
+
+def test_step_graph_failure_reports_like_direct(gpu, oracle, monkeypatch):
+    """A Newton failure inside a replayed step reports the oracle's message (the tags of the captured
+    enqueue are restored on every replay)."""
+    spec = P.config_c1(scale=1)
+    spec.problem.newton_max_iter = 1  # every cell hits the cap
+    o = opts(spec, 0, steps=1)
+    with pytest.raises(oracle.OracleError) as ce:
+        oracle.integrate(spec.problem, spec.phi0, o)
+    want = str(ce.value).split("] ", 1)[1]
+    ctx = api.GpuContext(spec.problem, spec.M, spec.convention)
+    try:
+        for _ in range(3):  # direct, captured, replayed
+            with pytest.raises(api.SolveError) as ge:
+                api.integrate(spec.problem, spec.phi0, o, ctx=ctx)
+            assert str(ge.value) == want
+    finally:
+        ctx.close()
