@@ -335,8 +335,9 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_tiled<true>(x + sbase, b + sbase, nx, ny, nz, z, ring, &aring, [](int) {},
-                   [&](int, unsigned cell, const double (&v)[3][5], double bv, bool ok) {
+  walk_tiled<!BMAX>(x + sbase, b + sbase, nx, ny, nz, z, ring, &aring, [](int) {},
+                   [&](int, unsigned cell, const double (&v)[3][5], double bva, bool ok) {
+                     const double bv = BMAX ? v[0][2] : bva;  // BMAX: x is b (the solve's first check)
                      // mg_ax_taps with the species coefficients hoisted (same expression)
                      double lap = 0.0;
                      lap = lap + cs0 * (-v[0][0] + 16.0 * v[0][1] - 30.0 * v[0][2] + 16.0 * v[0][3] - v[0][4]);
@@ -370,9 +371,11 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_pair(const __grid_constant_
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_pair<true, kMgRing, kMgRing - 2>(x + sbase, b + sbase, nx, ny, nz, z, mg_pring, mg_pring + kMgRing * kPPlaneSlot, [](int) {},
-                  [&](int, unsigned cell, const PairTaps& v, const double (&bv)[2], bool ok) {
+  walk_pair<!BMAX, kMgRing, kMgRing - 2>(x + sbase, b + sbase, nx, ny, nz, z, mg_pring, mg_pring + kMgRing * kPPlaneSlot, [](int) {},
+                  [&](int, unsigned cell, const PairTaps& v, const double (&bva)[2], bool ok) {
                     double xn[2];
+                    // BMAX: x is b (the solve's first check), so b comes from the x tile's centre taps
+                    const double bv[2] = {BMAX ? v.x[2] : bva[0], BMAX ? v.x[3] : bva[1]};
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                       double lap = 0.0;
@@ -406,9 +409,10 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_tma(const __grid_constant__
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_pair_tma<true, kTmaRing - 2>(maps, nx, ny, nz, z, mg_tring,
-                                    [&](int, unsigned cell, const PairTaps& v, const double (&bv)[2], bool) {
+  walk_pair_tma<!BMAX, kTmaRing - 2>(maps, nx, ny, nz, z, mg_tring,
+                                    [&](int, unsigned cell, const PairTaps& v, const double (&bva)[2], bool) {
                                       double xn[2];
+                                      const double bv[2] = {BMAX ? v.x[2] : bva[0], BMAX ? v.x[3] : bva[1]};
 #pragma unroll
                                       for (int c = 0; c < 2; ++c) {
                                         double lap = 0.0;
@@ -1042,7 +1046,7 @@ struct MgRunner {
     const double* xin = (l == 0 && first_x) ? first_x : Lv.x;
     if (l == 0) first_x = nullptr;
     const bool chk = l == 0 && check_next;
-    const bool bm = chk && first_check;
+    const bool bm = chk && first_check;  // the solve's first check: x is b (the BMAX kernels read b from the x tile)
     const bool tiled = DIM == 3 && !from_zero && tile3d_ok(Lv.ncell);
     const bool pair = tiled && Lv.nx % 2 == 0 && mg_pair_enabled();
     const double n8 = 8.0 * Lv.ncell * h.S;
