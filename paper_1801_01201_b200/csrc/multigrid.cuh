@@ -241,6 +241,10 @@ __global__ void k_mg_begin(int S, int* active, int* cycles, double* bmax, double
 
 // max of non-negative values, NaN ignored (the oracle's `if (r > m) m = r`)
 __device__ __forceinline__ double max_keep(double m, double r) { return r > m ? r : m; }
+// The running max of |v| kept as a signed value ms whose magnitude is max_keep's (|v| > |ms| ? v :
+// ms; NaN never wins): the compare takes both magnitudes as operand modifiers, so no |v| is
+// materialised per cell (an FP64 add on sm_100a).  The norm is fabs(ms).
+__device__ __forceinline__ double max_keep_abs(double ms, double v) { return fabs(v) > fabs(ms) ? v : ms; }
 
 // block max of m (and mb) -> one atomic per block into out[s] (bmax[s]); all threads participate
 template <bool BMAX>
@@ -346,10 +350,10 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
                      const double r = bv - (v[0][2] - coef * lap);
                      if (!ok) return;
                      if (SMOOTH) __stcg(xos + cell, v[2][2] + wd * r);
-                     if (NORM) m = max_keep(m, fabs(r));
-                     if (BMAX) mb = max_keep(mb, fabs(bv));
+                     if (NORM) m = max_keep_abs(m, r);
+                     if (BMAX) mb = max_keep_abs(mb, bv);
                    });
-  if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
+  if (NORM) block_max_atomic<BMAX>(fabs(m), fabs(mb), red, redb, out + z.s, bmax + z.s);
 }
 
 // The same level-0 sweep / check with two x-adjacent cells per thread (even nx; walk_pair): 128-bit
@@ -384,12 +388,12 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_pair(const __grid_constant_
                       lap = lap + cs2 * (-v.z[c][0] + 16.0 * v.z[c][1] - 30.0 * v.z[c][2] + 16.0 * v.z[c][3] - v.z[c][4]);
                       const double r = bv[c] - (v.x[c + 2] - coef * lap);
                       xn[c] = v.z[c][2] + wd * r;
-                      if (NORM) m = max_keep(m, ok ? fabs(r) : 0.0);
-                      if (BMAX) mb = max_keep(mb, ok ? fabs(bv[c]) : 0.0);
+                      if (NORM && ok) m = max_keep_abs(m, r);
+                      if (BMAX && ok) mb = max_keep_abs(mb, bv[c]);
                     }
                     if (SMOOTH && ok) __stcg(reinterpret_cast<double2*>(xos + cell), make_double2(xn[0], xn[1]));
                   });
-  if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
+  if (NORM) block_max_atomic<BMAX>(fabs(m), fabs(mb), red, redb, out + z.s, bmax + z.s);
 }
 
 // The same level-0 sweep / check with the planes staged by TMA (tma.cuh walk_pair_tma; whole 64 x 8
@@ -421,12 +425,12 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_tma(const __grid_constant__
                                         lap = lap + cs2 * (-v.z[c][0] + 16.0 * v.z[c][1] - 30.0 * v.z[c][2] + 16.0 * v.z[c][3] - v.z[c][4]);
                                         const double r = bv[c] - (v.x[c + 2] - coef * lap);
                                         xn[c] = v.z[c][2] + wd * r;
-                                        if (NORM) m = max_keep(m, fabs(r));
-                                        if (BMAX) mb = max_keep(mb, fabs(bv[c]));
+                                        if (NORM) m = max_keep_abs(m, r);
+                                        if (BMAX) mb = max_keep_abs(mb, bv[c]);
                                       }
                                       if (SMOOTH) __stcg(reinterpret_cast<double2*>(xos + cell), make_double2(xn[0], xn[1]));
                                     });
-  if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + z.s, bmax + z.s);
+  if (NORM) block_max_atomic<BMAX>(fabs(m), fabs(mb), red, redb, out + z.s, bmax + z.s);
 }
 
 // 2-D level sweep / check on the row-streaming walker (stencil2d.cuh; nx even): per cell the
@@ -456,12 +460,12 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_mg2_rows(const __grid_con
                       lap = lap + c1 * (-v.y[c][0] + 16.0 * v.y[c][1] - 30.0 * v.y[c][2] + 16.0 * v.y[c][3] - v.y[c][4]);
                       const double r = bv[c] - (v.x[c + 2] - coef * lap);
                       xn[c] = v.x[c + 2] + wd * r;
-                      if (NORM) m = max_keep(m, ok ? fabs(r) : 0.0);
-                      if (BMAX) mb = max_keep(mb, ok ? fabs(bv[c]) : 0.0);
+                      if (NORM && ok) m = max_keep_abs(m, r);
+                      if (BMAX && ok) mb = max_keep_abs(mb, bv[c]);
                     }
                     if (SMOOTH && ok) __stcg(reinterpret_cast<double2*>(xos + cell), make_double2(xn[0], xn[1]));
                   });
-  if (NORM) block_max_atomic<BMAX>(m, mb, red, redb, out + s, bmax + s);
+  if (NORM) block_max_atomic<BMAX>(fabs(m), fabs(mb), red, redb, out + s, bmax + s);
 }
 
 // launched on the COARSE grid
