@@ -340,11 +340,8 @@ int launch_react_sm(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   const int blocks = grid_of(ctx->g.ncell, 128);
   ctx->tm.before(kKReact, s);
   if constexpr (MODE == kModeMisdcq || MODE == kModeMisdc) {
-    switch (ctx->g.ndim) {
-      case 1: k_react<S, 1, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
-      case 2: k_react<S, 2, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
-      default: k_react<S, 3, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
-    }
+    if (a.fd_ad) k_react<S, 0, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
+    else k_react<S, 1, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);  // 1-D only
   } else {
     k_react<S, 1, MODE><<<blocks, 128, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
   }
@@ -369,11 +366,8 @@ template <int S, int MODE>
 void launch_fixup_sm(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   const dim3 grid(148), block(128);
   if constexpr (MODE == kModeMisdcq || MODE == kModeMisdc) {
-    switch (ctx->g.ndim) {
-      case 1: k_react_fixup<S, 1, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
-      case 2: k_react_fixup<S, 2, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
-      default: k_react_fixup<S, 3, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st); break;
-    }
+    if (a.fd_ad) k_react_fixup<S, 0, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
+    else k_react_fixup<S, 1, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
   } else {
     k_react_fixup<S, 1, MODE><<<grid, block, 0, s>>>(ctx->rx, ctx->ops, ctx->g, a, ctx->d_st);
   }
@@ -682,19 +676,13 @@ double QE(const cisdc_tables& t, int m, int j) { return t.QtE[m * t.M + j]; }
 
 // The reaction stage of MISDC/MISDCQ adds F_D(phi_AD[m+1]) (integrators.cpp:90,125: a separate
 // eval_diffusion in the reference too).  It is evaluated by the tiled stencil kernels into a
-// scratch field that the Newton kernel then reads pointwise, instead of a (4 ndim + 1)-tap stencil
-// per species inside the FP64-bound Newton kernel: C4 33.3 -> 22.4 ms of Newton per step for 4.2 ms
-// of evaluation.  1-D grids (L2-resident, launch-bound) keep the stencil inside
-// (CISDC_REACT_STENCIL=1: inside everywhere).
-bool react_fd_separate() {
-  static const bool v = [] {
-    const char* e = std::getenv("CISDC_REACT_STENCIL");
-    return !(e && e[0] == '1');
-  }();
-  return v;
-}
+// scratch field that the Newton kernel then reads pointwise (its DIM = 0 instantiation), instead of
+// a (4 ndim + 1)-tap stencil per species inside the FP64-bound Newton kernel: C4 33.3 -> 22.4 ms of
+// Newton per step for 4.2 ms of evaluation.  1-D grids (L2-resident, launch-bound) keep the
+// stencil inside.
+bool react_fd_separate(const cisdc_gpu_ctx* ctx) { return ctx->linear || ctx->g.ndim >= 2; }
 int prepare_fd_ad(cisdc_gpu_ctx* ctx, ReactArgs& a, cudaStream_t s) {
-  if (!ctx->linear && (!react_fd_separate() || ctx->g.ndim < 2)) return CISDC_OK;
+  if (!react_fd_separate(ctx)) return CISDC_OK;
   a.fd_ad = ctx->fd_ad[1];
   return launch_eval_ad(ctx, a.phi_ad, nullptr, ctx->fd_ad[1], s);
 }

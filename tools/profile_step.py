@@ -21,10 +21,12 @@ def main():
     ap.add_argument("--scale", type=int, default=2)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--workers", type=int, default=2)
+    ap.add_argument("--scheme", type=int, default=None)
     a = ap.parse_args()
     spec = problems.CONFIGS[a.config](scale=a.scale)
-    opt = api.IntegrateOptions(scheme=spec.scheme, dt=spec.dt, n_steps=1, M=spec.M, n_sweeps=spec.n_sweeps,
-                               nu=spec.nu, workers=a.workers if spec.scheme == 2 else 0)
+    scheme = spec.scheme if a.scheme is None else a.scheme
+    opt = api.IntegrateOptions(scheme=scheme, dt=spec.dt, n_steps=1, M=spec.M, n_sweeps=spec.n_sweeps,
+                               nu=spec.nu, workers=a.workers if scheme == 2 else 0)
     ctx = api.GpuContext(spec.problem, spec.M)
     for _ in range(a.steps):
         r = api.integrate(spec.problem, spec.phi0, opt, ctx=ctx)
