@@ -407,7 +407,7 @@ def mg_levels(p, coef):
     return L
 
 
-@pytest.mark.parametrize("n", [(128, 96, 1), (64, 32, 1), (64, 32, 48)])
+@pytest.mark.parametrize("n", [(128, 96, 1), (64, 32, 1), (64, 32, 48), (256, 192, 1)])
 def test_multigrid_hierarchy_bitwise(gpu, oracle, n):
     """Stiff diffusion (several multigrid levels: restriction, prolongation, coarse sweeps, the
     single-block coarse kernel) on 2-D and 3-D grids, C3's reaction chain: bitwise equal to the

@@ -1,9 +1,8 @@
 #!/bin/bash
 TAG=${1:-r2x}
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/${TAG}_gputest.log
-timeout 300 python bench.py > gpurun_out/${TAG}_bench_c5.log 2>&1
-timeout 300 python bench.py --scheme 1 --no-cpu-baseline --steps 3 > gpurun_out/${TAG}_bench_c5m.log 2>&1
-timeout 300 python bench.py --scheme 0 --no-cpu-baseline --steps 3 > gpurun_out/${TAG}_bench_c5d.log 2>&1
-timeout 300 python bench.py --config c4 --no-cpu-baseline > gpurun_out/${TAG}_bench_c4.log 2>&1
-timeout 300 python bench.py --config c4 --scheme 0 --no-cpu-baseline > gpurun_out/${TAG}_bench_c4d.log 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x -k "hierarchy or config_parity or full_size or cycle_cap or device_looped" > gpurun_out/${TAG}_gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/${TAG}_gputest.log
+for c in c3 c4; do
+timeout 300 python bench.py --config $c --no-cpu-baseline > gpurun_out/${TAG}_bench_$c.log 2>&1
+CISDC_MG_COARSE=1 timeout 300 python bench.py --config $c --no-cpu-baseline > gpurun_out/${TAG}_bench_${c}_cta.log 2>&1
+done
