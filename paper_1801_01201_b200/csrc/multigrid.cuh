@@ -100,7 +100,7 @@ __device__ __forceinline__ double mg_ax(const MgCoef& C, int s, const double* __
     const double g2 = mg_at(x, nx, ny, nz, i, j, k, a, 0);
     const double g3 = mg_at(x, nx, ny, nz, i, j, k, a, 1);
     const double g4 = mg_at(x, nx, ny, nz, i, j, k, a, 2);
-    lap = lap + C.c[s][a] * (-g0 + 16.0 * g1 - 30.0 * g2 + 16.0 * g3 - g4);
+    lap = lap + C.c[s][a] * lap5(g0, g1, g2, g3, g4);
   }
   return __ldg(x + ((long long)k * ny + j) * nx + i) - C.coef * lap;
 }
@@ -316,7 +316,7 @@ __device__ __forceinline__ double mg_ax_taps(const MgCoef& C, int s, const doubl
   double lap = 0.0;
 #pragma unroll
   for (int a = 0; a < 3; ++a)
-    lap = lap + C.c[s][a] * (-v[a][0] + 16.0 * v[a][1] - 30.0 * v[a][2] + 16.0 * v[a][3] - v[a][4]);
+    lap = lap + C.c[s][a] * lap5(v[a][0], v[a][1], v[a][2], v[a][3], v[a][4]);
   return v[0][2] - C.coef * lap;
 }
 
@@ -344,9 +344,9 @@ __global__ void __launch_bounds__(kTX* kTY, kMgMinBlocks) k_mg3_tiled(const __gr
                      const double bv = BMAX ? v[0][2] : bva;  // BMAX: x is b (the solve's first check)
                      // mg_ax_taps with the species coefficients hoisted (same expression)
                      double lap = 0.0;
-                     lap = lap + cs0 * (-v[0][0] + 16.0 * v[0][1] - 30.0 * v[0][2] + 16.0 * v[0][3] - v[0][4]);
-                     lap = lap + cs1 * (-v[1][0] + 16.0 * v[1][1] - 30.0 * v[1][2] + 16.0 * v[1][3] - v[1][4]);
-                     lap = lap + cs2 * (-v[2][0] + 16.0 * v[2][1] - 30.0 * v[2][2] + 16.0 * v[2][3] - v[2][4]);
+                     lap = lap + cs0 * lap5(v[0][0], v[0][1], v[0][2], v[0][3], v[0][4]);
+                     lap = lap + cs1 * lap5(v[1][0], v[1][1], v[1][2], v[1][3], v[1][4]);
+                     lap = lap + cs2 * lap5(v[2][0], v[2][1], v[2][2], v[2][3], v[2][4]);
                      const double r = bv - (v[0][2] - coef * lap);
                      if (!ok) return;
                      if (SMOOTH) __stcg(xos + cell, v[2][2] + wd * r);
@@ -383,9 +383,9 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_pair(const __grid_constant_
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                       double lap = 0.0;
-                      lap = lap + cs0 * (-v.x[c] + 16.0 * v.x[c + 1] - 30.0 * v.x[c + 2] + 16.0 * v.x[c + 3] - v.x[c + 4]);
-                      lap = lap + cs1 * (-v.y[c][0] + 16.0 * v.y[c][1] - 30.0 * v.y[c][2] + 16.0 * v.y[c][3] - v.y[c][4]);
-                      lap = lap + cs2 * (-v.z[c][0] + 16.0 * v.z[c][1] - 30.0 * v.z[c][2] + 16.0 * v.z[c][3] - v.z[c][4]);
+                      lap = lap + cs0 * lap5(v.x[c], v.x[c + 1], v.x[c + 2], v.x[c + 3], v.x[c + 4]);
+                      lap = lap + cs1 * lap5(v.y[c][0], v.y[c][1], v.y[c][2], v.y[c][3], v.y[c][4]);
+                      lap = lap + cs2 * lap5(v.z[c][0], v.z[c][1], v.z[c][2], v.z[c][3], v.z[c][4]);
                       const double r = bv[c] - (v.x[c + 2] - coef * lap);
                       xn[c] = v.z[c][2] + wd * r;
                       if (NORM && ok) m = max_keep_abs(m, r);
@@ -420,9 +420,9 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_tma(const __grid_constant__
 #pragma unroll
                                       for (int c = 0; c < 2; ++c) {
                                         double lap = 0.0;
-                                        lap = lap + cs0 * (-v.x[c] + 16.0 * v.x[c + 1] - 30.0 * v.x[c + 2] + 16.0 * v.x[c + 3] - v.x[c + 4]);
-                                        lap = lap + cs1 * (-v.y[c][0] + 16.0 * v.y[c][1] - 30.0 * v.y[c][2] + 16.0 * v.y[c][3] - v.y[c][4]);
-                                        lap = lap + cs2 * (-v.z[c][0] + 16.0 * v.z[c][1] - 30.0 * v.z[c][2] + 16.0 * v.z[c][3] - v.z[c][4]);
+                                        lap = lap + cs0 * lap5(v.x[c], v.x[c + 1], v.x[c + 2], v.x[c + 3], v.x[c + 4]);
+                                        lap = lap + cs1 * lap5(v.y[c][0], v.y[c][1], v.y[c][2], v.y[c][3], v.y[c][4]);
+                                        lap = lap + cs2 * lap5(v.z[c][0], v.z[c][1], v.z[c][2], v.z[c][3], v.z[c][4]);
                                         const double r = bv[c] - (v.x[c + 2] - coef * lap);
                                         xn[c] = v.z[c][2] + wd * r;
                                         if (NORM) m = max_keep_abs(m, r);
@@ -456,8 +456,8 @@ __global__ void __launch_bounds__(kRowWarps * 32, 2) k_mg2_rows(const __grid_con
 #pragma unroll
                     for (int c = 0; c < 2; ++c) {
                       double lap = 0.0;
-                      lap = lap + c0 * (-v.x[c] + 16.0 * v.x[c + 1] - 30.0 * v.x[c + 2] + 16.0 * v.x[c + 3] - v.x[c + 4]);
-                      lap = lap + c1 * (-v.y[c][0] + 16.0 * v.y[c][1] - 30.0 * v.y[c][2] + 16.0 * v.y[c][3] - v.y[c][4]);
+                      lap = lap + c0 * lap5(v.x[c], v.x[c + 1], v.x[c + 2], v.x[c + 3], v.x[c + 4]);
+                      lap = lap + c1 * lap5(v.y[c][0], v.y[c][1], v.y[c][2], v.y[c][3], v.y[c][4]);
                       const double r = bv[c] - (v.x[c + 2] - coef * lap);
                       xn[c] = v.x[c + 2] + wd * r;
                       if (NORM && ok) m = max_keep_abs(m, r);
@@ -576,8 +576,8 @@ __global__ void __launch_bounds__(256) k_mg_restrict2_pair(const __grid_constant
       const double* yy = dx == 0 ? ya : yb;
       const double xcc = g[2 + dx];
       double lap = 0.0;
-      lap = lap + C.c[s][0] * (-g[dx] + 16.0 * g[dx + 1] - 30.0 * xcc + 16.0 * g[dx + 3] - g[dx + 4]);
-      lap = lap + C.c[s][1] * (-yy[0] + 16.0 * yy[1] - 30.0 * xcc + 16.0 * yy[2] - yy[3]);
+      lap = lap + C.c[s][0] * lap5(g[dx], g[dx + 1], xcc, g[dx + 3], g[dx + 4]);
+      lap = lap + C.c[s][1] * lap5(yy[0], yy[1], xcc, yy[2], yy[3]);
       const double ax = xcc - C.coef * lap;
       acc = acc + ((dx == 0 ? bv.x : bv.y) - ax);
     }

@@ -23,8 +23,11 @@ __device__ __forceinline__ double at_off(const double* __restrict__ f, const Geo
   return __ldg(f + ((long long)k * g.ny + j) * g.nx + i);
 }
 
+// The reference's stencil -g0 + 16 g1 - 30 g2 + 16 g3 - g4 (reaction_diffusion.cpp:97), evaluated left
+// to right.  16 g is exact (a power of two; |g| < 2^1019), so round(16 g1 + (-g0)) is one fused
+// multiply-add, and likewise the + 16 g3 term: the same bits with 5 FP64 operations instead of 7.
 __device__ __forceinline__ double lap5(double g0, double g1, double g2, double g3, double g4) {
-  return -g0 + 16.0 * g1 - 30.0 * g2 + 16.0 * g3 - g4;
+  return __fma_rn(16.0, g3, __fma_rn(16.0, g1, -g0) - 30.0 * g2) - g4;
 }
 
 template <int DIM>
