@@ -44,7 +44,7 @@ constexpr int kPhi = 0, kFa = 1, kFd = 2, kFr = 3;
 
 const char* kClassNames[kNumKernelClasses] = {"quad_base", "rhs", "solve1d", "mg_smooth", "mg_restrict",
                                               "mg_prolong", "mg_norm", "react_newton", "eval_ad", "eval_r",
-                                              "increment"};
+                                              "increment", "react_newton_rhs"};
 
 // Launch accounting + optional live CUDA-event timing per kernel class.
 struct Timing final : LaunchHook {
@@ -384,7 +384,11 @@ void launch_fixup_m(cisdc_gpu_ctx* ctx, const ReactArgs& a, cudaStream_t s) {
   }
 }
 
-int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a_in, cudaStream_t s) {
+double rhs_fields(const RhsArgs& a);
+
+// next: the right-hand side of the following diffusion cell, assembled by the same kernel
+// (k_react_next; the network-specialised CISDCQ kernel only -- see can_fuse_next_rhs)
+int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a_in, cudaStream_t s, const RhsArgs* next = nullptr) {
   if (ctx->linear && 1.0 - a_in.coef * ctx->lin_r == 0.0)
     return set_err(ctx, CISDC_E_SOLVE, "LinearScalarProblem: singular reaction stage");
   ReactArgs a = a_in;
@@ -397,11 +401,17 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a_in, cudaStream
     aa.defer_list = ctx->defer_list;
     aa.defer_count = ctx->defer_count;
     DevStatus* st = ctx->d_st;
-    void* args[5] = {&rx, &o, &g, &aa, &st};
-    ctx->tm.before(kKReact, s);
-    CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[mode]), dim3(grid_of(ctx->g.ncell, 128)), dim3(128),
-                        args, 0, s));
-    ctx->tm.after(kKReact, s, F8(ctx) * react_fields(mode, a));
+    RhsArgs nx{};
+    if (next) {
+      nx = *next;
+      nx.wild = ctx->ops.wild;
+    }
+    void* args[6] = {&rx, &o, &g, &aa, &st, &nx};
+    const int cls = next ? kKReactRhs : kKReact;
+    ctx->tm.before(cls, s);
+    CU(cudaLaunchKernel(reinterpret_cast<const void*>(ctx->rtc.fn[next ? 4 : mode]), dim3(grid_of(ctx->g.ncell, 128)),
+                        dim3(128), args, 0, s));
+    ctx->tm.after(cls, s, F8(ctx) * (react_fields(mode, a) + (next ? rhs_fields(nx) : 0.0)));
     // cells whose LU needed a row interchange: dense generic kernel, then reset the list
     ctx->tm.before(kKReact, s);
     switch (mode) {
@@ -415,6 +425,7 @@ int launch_react(cisdc_gpu_ctx* ctx, int mode, const ReactArgs& a_in, cudaStream
     CU(cudaMemsetAsync(ctx->defer_count, 0, sizeof(int), s));
     return CISDC_OK;
   }
+  if (next) return set_err(ctx, CISDC_E_INVALID_ARGUMENT, "launch_react: fused next rhs needs the specialised kernel");
   switch (mode) {
     case kModeMisdcq: return launch_react_m<kModeMisdcq>(ctx, a, s);
     case kModeMisdc: return launch_react_m<kModeMisdc>(ctx, a, s);
@@ -430,7 +441,8 @@ double distinct_fields(std::vector<const void*> p) {
   return (double)(std::unique(p.begin(), p.end()) - p.begin());
 }
 
-int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
+// compulsory fields (distinct inputs + outputs) of one stage right-hand side
+double rhs_fields(const RhsArgs& a) {
   std::vector<const void*> in;
   if (a.kind == kRhsMisdc) {
     in.push_back(a.phim);
@@ -448,7 +460,11 @@ int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
   in.insert(in.end(), {a.X, a.Y, a.Z});
   double outs = 1 + (a.out2 != nullptr) + (a.base_out != nullptr);
   for (int t = 0; t < a.nt; ++t) outs += (a.t[t].outA != nullptr) + (a.t[t].outDR != nullptr);
-  const double fields = distinct_fields(in) + outs;
+  return distinct_fields(in) + outs;
+}
+
+int launch_rhs(cisdc_gpu_ctx* ctx, const RhsArgs& a, cudaStream_t s) {
+  const double fields = rhs_fields(a);
   RhsArgs aw = a;
   aw.wild = ctx->ops.wild;
   ctx->tm.before(kKRhs, s);
@@ -935,7 +951,10 @@ int diffusion_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt
 }
 
 // cisdcq_cells::run_reaction_cell (integrators.cpp:237-258)
-int reaction_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c) {
+// next_rhs: the right-hand side of D(m+1, ell), assembled by this cell's Newton kernel; ev_newton is
+// recorded right after that kernel (the D stream waits on it instead of on the whole cell)
+int reaction_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt, cudaStream_t s, cisdc_counters* c,
+                  const RhsArgs* next_rhs = nullptr, cudaEvent_t ev_newton = nullptr) {
   const int prev = ctx->cur, row = m - 1;
   ReactArgs a{};
   a.coef = dt * QI(ctx->tb, row, m - 1);
@@ -949,10 +968,20 @@ int reaction_cell(cisdc_gpu_ctx* ctx, const Slots& W, int m, int ell, double dt,
   a.p0 = W.get(0, m, ell);
   a.phi_out = W.get(1, m, ell);
   a.fr_out = W.get(4, m, ell);
-  TRY(launch_react(ctx, kModeCisdcq, a, s));
+  TRY(launch_react(ctx, kModeCisdcq, a, s, next_rhs));
+  if (ev_newton) CU(cudaEventRecord(ev_newton, s));
   if (c) ++c->reaction;
   TRY(launch_eval_ad(ctx, a.phi_out, W.get(2, m, ell), W.get(3, m, ell), s));
   return CISDC_OK;
+}
+
+// k_react_next serves the NVRTC-specialised mass-action kernel (CISDC_FUSE_RHS=0: separate k_rhs)
+bool can_fuse_next_rhs(const cisdc_gpu_ctx* ctx) {
+  static const bool env_on = [] {
+    const char* e = std::getenv("CISDC_FUSE_RHS");
+    return !e || std::atoi(e) != 0;
+  }();
+  return env_on && ctx->rtc.ready && !ctx->trace_on;
 }
 
 // cisdcq_sweep (workers == 0, integrators.cpp:273-288) or execute_pipelined (pipeline.cpp:171-320)
@@ -967,11 +996,19 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   // base row 0 (read by D(1, ell) alone) is then not stored when nu == 1
   const RhsArgs r11 = diffusion_rhs(ctx, W, 1, 1, dt);
   TRY(launch_quad_base(ctx, ctx->cur, dt, sd, &r11, nu == 1));
+  // R(m, ell)'s Newton kernel also assembles D(m+1, ell)'s right-hand side (k_react_next): the
+  // network-specialised kernel only; off while a schedule trace is recorded (the D cell's rhs would
+  // run inside the R cell's interval)
+  const bool fuse = can_fuse_next_rhs(ctx);
+  RhsArgs nr{};
   if (workers <= 0) {
+    bool ready = true;  // D(1, 1): the quadrature pass
     for (int ell = 1; ell <= nu; ++ell)
       for (int m = 1; m <= M; ++m) {
-        TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c, m == 1 && ell == 1));
-        TRY(reaction_cell(ctx, W, m, ell, dt, sd, c));
+        TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c, ready));
+        ready = fuse && m < M;
+        if (ready) nr = diffusion_rhs(ctx, W, m + 1, ell, dt);
+        TRY(reaction_cell(ctx, W, m, ell, dt, sd, c, ready ? &nr : nullptr));
       }
     return CISDC_OK;
   }
@@ -980,13 +1017,15 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   // D cells are totally ordered on their stream (single rhs buffer); R cells write only their slots.
   cudaStream_t sr = ctx->s_r;
   const size_t ncells = (size_t)M * nu;
-  while (ctx->ev_pool.size() < 2 * ncells) {
+  while (ctx->ev_pool.size() < 3 * ncells) {
     cudaEvent_t e;
     CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     ctx->ev_pool.push_back(e);
   }
-  auto evD = [&](int m, int ell) { return ctx->ev_pool[2 * ((size_t)(ell - 1) * M + (m - 1))]; };
-  auto evR = [&](int m, int ell) { return ctx->ev_pool[2 * ((size_t)(ell - 1) * M + (m - 1)) + 1]; };
+  auto evD = [&](int m, int ell) { return ctx->ev_pool[3 * ((size_t)(ell - 1) * M + (m - 1))]; };
+  auto evR = [&](int m, int ell) { return ctx->ev_pool[3 * ((size_t)(ell - 1) * M + (m - 1)) + 1]; };
+  // after R(m, ell)'s Newton kernel, which wrote D(m+1, ell)'s right-hand side (fuse)
+  auto evN = [&](int m, int ell) { return ctx->ev_pool[3 * ((size_t)(ell - 1) * M + (m - 1)) + 2]; };
   // trace: start/end events of cell id (TaskGraph::cell_id = 2 ((ell-1) M + (m-1)) + kind)
   const bool tr = ctx->trace_on;
   if (tr) {
@@ -1005,6 +1044,7 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
   };
   CU(cudaEventRecord(ctx->ev_base, sd));
   CU(cudaStreamWaitEvent(sr, ctx->ev_base, 0));
+  bool ready = true;  // D(1, 1): the quadrature pass
   for (int ell = 1; ell <= nu; ++ell) {
     for (int m = 1; m <= M; ++m) {
       if (m >= 3) CU(cudaStreamWaitEvent(sd, evR(m - 2, ell), 0));
@@ -1012,13 +1052,16 @@ int sweep_cisdcq(cisdc_gpu_ctx* ctx, double dt, int nu, int workers, cisdc_count
         if (m >= 2) CU(cudaStreamWaitEvent(sd, evR(m - 1, ell - 1), 0));
         CU(cudaStreamWaitEvent(sd, evR(m, ell - 1), 0));
       }
+      if (ready && m >= 2) CU(cudaStreamWaitEvent(sd, evN(m - 1, ell), 0));
       if (tr) CU(cudaEventRecord(tev(0, m, ell, 0), sd));
-      TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c, m == 1 && ell == 1));
+      TRY(diffusion_cell(ctx, W, m, ell, dt, sd, c, ready));
       if (tr) CU(cudaEventRecord(tev(0, m, ell, 1), sd));
       CU(cudaEventRecord(evD(m, ell), sd));
       CU(cudaStreamWaitEvent(sr, evD(m, ell), 0));
       if (tr) CU(cudaEventRecord(tev(1, m, ell, 0), sr));
-      TRY(reaction_cell(ctx, W, m, ell, dt, sr, c));
+      ready = fuse && m < M;
+      if (ready) nr = diffusion_rhs(ctx, W, m + 1, ell, dt);
+      TRY(reaction_cell(ctx, W, m, ell, dt, sr, c, ready ? &nr : nullptr, ready ? evN(m, ell) : nullptr));
       if (tr) CU(cudaEventRecord(tev(1, m, ell, 1), sr));
       CU(cudaEventRecord(evR(m, ell), sr));
     }

@@ -91,7 +91,8 @@ enum KernelClass {
   kKEvalAD = 8,    // k_eval_ad
   kKEvalR = 9,     // k_eval_r
   kKIncr = 10,     // k_incr_*
-  kNumKernelClasses = 11
+  kKReactRhs = 11,  // k_react_next (Newton of R(m, l) + the right-hand side of D(m+1, l))
+  kNumKernelClasses = 12
 };
 
 #ifndef __CUDACC_RTC__

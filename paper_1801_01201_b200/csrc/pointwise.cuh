@@ -11,6 +11,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "rhs.cuh"
 
 namespace cisdc_b200 {
 
@@ -52,60 +53,6 @@ __global__ void __launch_bounds__(256) k_quad_base(const __grid_constant__ QuadA
   }
   if (q.rhs0_kind == 1) q.rhs0[e] = acc0 - q.fc * q.X[e];
   else if (q.rhs0_kind == 2) q.rhs0[e] = acc0 + (q.fc * (q.X[e] - q.Y[e]) - q.fc * q.Z[e]);
-}
-
-// One correction term: cE*(A - Ap) + cI*(D - Dp)                 (R == nullptr)
-//                   or cE*(A - Ap) + cI*(D - Dp + R - Rp)
-// CISDCQ difference cache: a term whose differences dA = A - Ap and dDR = ((D - Dp) + R) - Rp were
-// stored by an earlier launch reads just those (diff != 0: D = dDR, dA = the cached dA or null); a
-// term read in full can store them (outA/outDR) for the later nodes.  Same operations, same bits.
-//
-// Exact zeros (skipA): in the literal Euler convention the configs use, QtE(m, j) is non-zero only
-// on the subdiagonal (reference quadrature.cpp:137-139), so most terms have cE == 0.0.  For finite
-// A - Ap, cE * (A - Ap) is then a signed zero, and t = (+-0) + tI equals tI bit for bit whenever
-// tI = cI * (...) != 0.  Such a term skips the A / Ap reads (and the dA cache): A and Ap are read
-// only at the elements where tI is itself a zero (the sign of the sum then depends on both), and
-// everywhere once an F_A evaluation flagged a value >= 2^1022, an Inf or a NaN (Ops::wild), where
-// the difference could overflow or carry a NaN.  A and Ap are always the original fields.
-struct RhsTerm {
-  double cE, cI;
-  const double *A, *Ap, *D, *Dp, *R, *Rp;
-  const double* dA;  // cached A - Ap (diff terms whose cE != 0)
-  int diff;
-  int skipA;
-  double *outA, *outDR;
-};
-
-enum RhsKind {
-  kRhsMisdcq = 0,  // out = base + sum(AD terms) - fc*X ; out2 = base + sum(ADR terms)
-  kRhsCisdcq = 1,  // out = base + sum(ADR terms) + (fc*(X - Y) - fc*Z)
-  kRhsMisdc = 2,   // base = phi_m + sum_j sc_j*(fa+fd+fr)_j ; out = base + fc*(X - Y - Z)
-  kRhsImexq = 3    // out = base + sum(ADR terms) - fc*(X + Y)   (imexq_sweep, integrators.cpp:155-164)
-};
-
-struct RhsArgs {
-  int kind;
-  int nt;
-  RhsTerm t[kMaxM];
-  double fc;
-  const double *X, *Y, *Z;
-  const double* base;  // kRhsMisdcq / kRhsCisdcq
-  double* out;
-  double* out2;        // kRhsMisdcq: reaction-stage partial rhs (may be null)
-  // kRhsMisdc
-  int M;
-  double sc[kMaxM + 1];
-  const double* phim;
-  const double *sfa[kMaxM + 1], *sfd[kMaxM + 1], *sfr[kMaxM + 1];
-  double* base_out;
-  const int* wild;  // Ops::wild of the context
-};
-
-// cE * (A - Ap) + tI with the skipA shortcut above
-__device__ __forceinline__ double rhs_term_a(const RhsTerm& T, long long e, double tI, bool skip) {
-  if (skip && tI != 0.0) return tI;
-  const double dA = (T.diff && T.dA) ? T.dA[e] : T.A[e] - T.Ap[e];
-  return T.cE * dA + tI;
 }
 
 __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, long long n) {
