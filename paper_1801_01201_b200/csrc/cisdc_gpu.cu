@@ -255,6 +255,13 @@ bool eval_pair() {
   return v;
 }
 
+// TMA-staged planes for F_A/F_D on whole-tile 3-D grids (CISDC_EVAL_TMA=0: the cp.async pair walker);
+// read per launch so that a process can compare the two (tests do)
+bool eval_tma() {
+  const char* e = std::getenv("CISDC_EVAL_TMA");
+  return !(e && e[0] == '0') && tma_encoder() != nullptr;
+}
+
 int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd, cudaStream_t s) {
   const Geom& g = ctx->g;
   if (ctx->linear) {
@@ -282,7 +289,18 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
         k_eval_ad<3><<<grid, block, 0, s>>>(ctx->ops, g, phi, fa, fd);
         break;
       }
-      if (g.nx % 2 == 0 && eval_pair()) {
+      TmaMaps maps;
+      if (g.nx % 2 == 0 && eval_pair() && tma_grid_ok(g.nx, g.ny, g.nz, g.ncell) && eval_tma() &&
+          tma_maps(maps, phi, nullptr, g.nx, g.ny, g.nz * g.S)) {
+        CU(func_attr_once(k_eval_ad3_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaEvalSmem));
+        CU(func_attr_once(k_eval_ad3_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaEvalSmem));
+        if (ctx->ops.vconst)
+          k_eval_ad3_tma<true><<<tile3d_pair_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), kTmaEvalSmem, s>>>(
+              ctx->ops, g, maps, fa, fd, kZChunk);
+        else
+          k_eval_ad3_tma<false><<<tile3d_pair_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), kTmaEvalSmem, s>>>(
+              ctx->ops, g, maps, fa, fd, kZChunk);
+      } else if (g.nx % 2 == 0 && eval_pair()) {
         CU(func_attr_once(k_eval_ad3_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
         CU(func_attr_once(k_eval_ad3_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
         if (ctx->ops.vconst)

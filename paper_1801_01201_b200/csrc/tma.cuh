@@ -12,9 +12,11 @@
 // (arrive.expect_tx by the producer, complete_tx by the copies, try_wait.parity by all threads);
 // the per-plane __syncthreads of the walker stays as the slot-reuse (WAR) fence.
 //
-// Shared-memory plane slot (doubles; every region 128-byte aligned, as the bulk tensor copy needs):
-//   [0, 512)    interior rows 0..7, pitch 64
-//   [512, 640)  rows -2, -1, pitch 64
+// Shared-memory plane slot (doubles; every region 128-byte aligned, as the bulk tensor copy needs;
+// rows -2 .. 9 are contiguous at pitch 64, so a thread's five y taps and its centre are one base
+// register plus compile-time offsets):
+//   [0, 128)    rows -2, -1, pitch 64
+//   [128, 640)  interior rows 0..7, pitch 64
 //   [640, 768)  rows 8, 9, pitch 64
 //   [768, 784)  columns -2, -1 of rows 0..7, pitch 2
 //   [784, 800)  columns 64, 65 of rows 0..7, pitch 2
@@ -32,12 +34,13 @@
 
 namespace cisdc_b200 {
 
-constexpr int kTmaMain = 0, kTmaTop = 512, kTmaBot = 640, kTmaLeft = 768, kTmaRight = 784;
+constexpr int kTmaTop = 0, kTmaMain = 128, kTmaBot = 640, kTmaLeft = 768, kTmaRight = 784;
 constexpr int kTmaSlot = 800;                               // doubles per plane slot
 constexpr unsigned kTmaPlaneBytes = kTmaSlot * 8u;          // 6400 bytes of x per plane
 constexpr unsigned kTmaAuxBytes = kPTX * kTY * 8u;          // 4096 bytes of rhs per plane
 constexpr int kTmaRing = 6;
-constexpr size_t kTmaSmem = (size_t)kTmaRing * (kTmaSlot + kPTX * kTY) * sizeof(double) + 128;
+constexpr size_t kTmaSmem = (size_t)kTmaRing * (kTmaSlot + kPTX * kTY) * sizeof(double) + 64 + 128;
+constexpr size_t kTmaEvalSmem = (size_t)kTmaRing * kTmaSlot * sizeof(double) + 64 + 128;  // no rhs ring
 
 // The tensor maps one walk needs: x with the three box shapes, and the rhs (interior box).
 struct TmaMaps {
@@ -62,6 +65,16 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// one lane of a converged warp (warp-uniform branch around it): straight-line UTMALDG issue
+__device__ __forceinline__ bool elect_one() {
+  unsigned pred;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, int x, int y, int z, unsigned bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
@@ -70,119 +83,170 @@ __device__ __forceinline__ void tma_load3(unsigned dst, const CUtensorMap* map, 
       : "memory");
 }
 
+// 128-bit shared load at a 32-bit shared-space address plus a compile-time byte offset (LDS.128 with
+// an immediate: a pointer rounded up through an integer loses its address space and compiles to
+// generic loads with 64-bit address arithmetic).  volatile: stays behind the mbarrier wait.
+template <int IMM>
+__device__ __forceinline__ void lds2(unsigned addr, double& a, double& b) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2+%3];" : "=d"(a), "=d"(b) : "r"(addr), "n"(IMM));
+}
+
 // walk_pair's contract (stencil3d.cuh) on TMA-staged planes; HAS_AUX stages the rhs (z-folded field
-// index s * nz + k).  The plane(k) hook of walk_pair is not needed by the multigrid kernels.
-template <bool HAS_AUX, int AHEAD, class Body>
+// index s * nz + k).  plane(k) runs once per plane before the body, as in walk_pair.
+//
+// The plane loop is unrolled by the ring size (6) and the z taps sit in a 6-deep register queue, so
+// inside the unrolled body every ring slot, mbarrier and phase parity is a compile-time constant:
+// plane k0 - 2 + j lives in slot j % 6 and is that slot's (j / 6)-th fill.  Staging distance 4:
+// the step of plane k waits for plane k + 2 and stages plane k + 4 into the slot of plane k - 2.
+template <bool HAS_AUX, class PlaneFn, class Body>
 __device__ __forceinline__ void walk_pair_tma(const TmaMaps& maps, int nx, int ny, int nz, const ZChunk& z,
-                                              double* smem, Body body) {
-  static_assert(AHEAD >= 4 && AHEAD + 2 <= kTmaRing, "ring too small for the staging distance");
+                                              double* smem, PlaneFn plane, Body body) {
+  static_assert(kTmaRing == 6, "the unrolled walker is written for a 6-slot ring");
+  constexpr int kSlotB = kTmaSlot * 8, kAuxB = kPTX * kTY * 8;
   const int i0 = blockIdx.x * kPTX, j0 = blockIdx.y * kTY;
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int t = ty * kTX + tx;
   const unsigned pl = (unsigned)nx * (unsigned)ny;
   const unsigned col = (unsigned)(j0 + ty) * (unsigned)nx + (unsigned)(i0 + 2 * tx);
-  // ring: kTmaRing x-slots, then kTmaRing rhs slots, then the mbarriers (base rounded up to the
-  // 128 bytes the bulk tensor copies need; kTmaSmem has the slack)
-  smem = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem) + 127) & ~static_cast<uintptr_t>(127));
-  double* xring = smem;
-  double* aring = smem + kTmaRing * kTmaSlot;
-  const unsigned xs = (unsigned)__cvta_generic_to_shared(xring);
-  const unsigned as = (unsigned)__cvta_generic_to_shared(aring);
-  const unsigned bars = (unsigned)__cvta_generic_to_shared(aring + kTmaRing * kPTX * kTY);
+  // ring: 6 x-slots, then 6 rhs slots, then the mbarriers (base rounded up to the 128 bytes the bulk
+  // tensor copies need; kTmaSmem has the slack)
+  const unsigned xs = ((unsigned)__cvta_generic_to_shared(smem) + 127u) & ~127u;
+  const unsigned as = xs + kTmaRing * kSlotB;
+  const unsigned bars = as + (HAS_AUX ? kTmaRing * kAuxB : 0);  // no rhs ring without a rhs
   const int zoff = z.s * nz;
   const int jt = j0 - 2 < 0 ? j0 - 2 + ny : j0 - 2;   // rows -2, -1 (wrapped)
   const int jb = j0 + kTY >= ny ? j0 + kTY - ny : j0 + kTY;  // rows 8, 9 (wrapped)
   const int il = i0 - 2 < 0 ? i0 - 2 + nx : i0 - 2;   // columns -2, -1
   const int ir = i0 + kPTX >= nx ? i0 + kPTX - nx : i0 + kPTX;  // columns 64, 65
   if (t == 0) {
+#pragma unroll
     for (int r = 0; r < kTmaRing; ++r) mbar_init(bars + 8u * r, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  auto issue = [&](int kk) {
-    if (t != 0 || kk > z.k1 + 1) return;
-    const int r = ring_slot<kTmaRing>(kk);
-    const unsigned bar = bars + 8u * r;
+  // stage plane kk into slot R (compile-time)
+  auto issue = [&](auto slot, int kk) {
+    constexpr int R = decltype(slot)::value;
+    if (ty != 0 || kk > z.k1 + 1) return;  // warp 0 stages (a warp is one tile row)
+    if (!elect_one()) return;
+    const unsigned bar = bars + 8u * R;
     const bool aux = HAS_AUX && kk >= z.k0 && kk < z.k1;
     mbar_expect_tx(bar, kTmaPlaneBytes + (aux ? kTmaAuxBytes : 0u));
     const int zz = zoff + wrapi(kk, nz);
-    const unsigned d = xs + (unsigned)(r * kTmaSlot) * 8u;
+    const unsigned d = xs + (unsigned)(R * kSlotB);
     tma_load3(d + kTmaMain * 8u, &maps.x_main, i0, j0, zz, bar);
     tma_load3(d + kTmaTop * 8u, &maps.x_rows, i0, jt, zz, bar);
     tma_load3(d + kTmaBot * 8u, &maps.x_rows, i0, jb, zz, bar);
     tma_load3(d + kTmaLeft * 8u, &maps.x_cols, il, j0, zz, bar);
     tma_load3(d + kTmaRight * 8u, &maps.x_cols, ir, j0, zz, bar);
-    if (aux) tma_load3(as + (unsigned)(r * kPTX * kTY) * 8u, &maps.b_main, i0, j0, zz, bar);
+    if (aux) tma_load3(as + (unsigned)(R * kAuxB), &maps.b_main, i0, j0, zz, bar);
   };
-  // per-slot phase bits (every thread tracks the same sequence of completions)
-  unsigned phase = 0;
-  auto wait = [&](int kk) {
-    const int r = ring_slot<kTmaRing>(kk);
-    mbar_wait(bars + 8u * r, (phase >> r) & 1u);
-    phase ^= 1u << r;
-  };
-  // this thread's tap addresses inside a slot (doubles): x taps (pairs at c-2, c, c+2), y taps
-  // (rows ty-2 .. ty+2 at column c), centre
+  // this thread's tap addresses inside slot 0 (shared-space bytes): x taps (pairs at c-2, c, c+2),
+  // y taps (rows ty-2 .. ty+2 at column c), its rhs pair
   const int c = 2 * tx;
-  const int ox0 = tx == 0 ? kTmaLeft + 2 * ty : kTmaMain + ty * kPTX + c - 2;
-  const int oxc = kTmaMain + ty * kPTX + c;
-  const int ox2 = tx == kTX - 1 ? kTmaRight + 2 * ty : kTmaMain + ty * kPTX + c + 2;
-  int oy[5];
+  const unsigned ax0 = xs + 8u * (unsigned)(tx == 0 ? kTmaLeft + 2 * ty : kTmaMain + ty * kPTX + c - 2);
+  const unsigned ay0 = xs + 8u * (unsigned)(kTmaTop + ty * kPTX + c);  // row ty - 2; row ty + o - 2 at + o * kRowB
+  const unsigned ax2 = xs + 8u * (unsigned)(tx == kTX - 1 ? kTmaRight + 2 * ty : kTmaMain + ty * kPTX + c + 2);
+  constexpr int kRowB = kPTX * 8, kCtr = 2 * kRowB;  // the centre pair sits at ay0 + kCtr
+  const unsigned aa = as + 16u * (unsigned)t;
+  issue(Phase<0>{}, z.k0 - 2);
+  issue(Phase<1>{}, z.k0 - 1);
+  issue(Phase<2>{}, z.k0);
+  issue(Phase<3>{}, z.k0 + 1);
+  issue(Phase<4>{}, z.k0 + 2);
+  issue(Phase<5>{}, z.k0 + 3);
+  double q[2][6];  // z taps: planes k-2 .. k+2 of phase P sit in q[.][(P + o) % 6]
 #pragma unroll
-  for (int o = 0; o < 5; ++o) {
-    const int rr = ty + o - 2;
-    oy[o] = rr < 0 ? kTmaTop + (rr + 2) * kPTX + c : (rr >= kTY ? kTmaBot + (rr - kTY) * kPTX + c : kTmaMain + rr * kPTX + c);
-  }
-  auto ld2 = [&](const double* p, double& a, double& b) {
-    const double2 v = *reinterpret_cast<const double2*>(p);
-    a = v.x;
-    b = v.y;
-  };
-#pragma unroll
-  for (int kk = -2; kk < AHEAD; ++kk) issue(z.k0 + kk);
-  double q[2][5];
-  for (int kk = -2; kk < 2; ++kk) wait(z.k0 + kk);
-#pragma unroll
-  for (int o = 0; o < 4; ++o) ld2(xring + ring_slot<kTmaRing>(z.k0 + o - 2) * kTmaSlot + oxc, q[0][o], q[1][o]);
-  auto step = [&](auto ph, int k) {
+  for (int r = 0; r < 4; ++r) mbar_wait(bars + 8u * r, 0u);
+  lds2<0 * kSlotB + kCtr>(ay0, q[0][0], q[1][0]);
+  lds2<1 * kSlotB + kCtr>(ay0, q[0][1], q[1][1]);
+  lds2<2 * kSlotB + kCtr>(ay0, q[0][2], q[1][2]);
+  lds2<3 * kSlotB + kCtr>(ay0, q[0][3], q[1][3]);
+  // phase P of iteration it handles plane k = k0 + 6 it + P = fill it of slot (P + 2) % 6
+  auto step = [&](auto ph, int k, unsigned par) {
     constexpr int P = decltype(ph)::value;
-    wait(k + 2);      // plane k+2 has landed
-    __syncthreads();  // every thread is past plane k-1: the slot of plane k+AHEAD-kTmaRing is free
-    issue(k + AHEAD);
-    const double* tk = xring + ring_slot<kTmaRing>(k) * kTmaSlot;
-    ld2(xring + ring_slot<kTmaRing>(k + 2) * kTmaSlot + oxc, q[0][(P + 4) % 5], q[1][(P + 4) % 5]);
+    constexpr int SK = (P + 2) % 6;   // slot of plane k
+    constexpr int S2 = (P + 4) % 6;   // slot of plane k + 2: fill it + (P >= 2)
+    mbar_wait(bars + 8u * S2, par ^ (P >= 2 ? 1u : 0u));  // plane k+2 has landed
+    __syncthreads();  // every thread is past plane k-1: the slot of plane k-2 is free
+    issue(Phase<P>{}, k + 4);
+    lds2<S2 * kSlotB + kCtr>(ay0, q[0][(P + 4) % 6], q[1][(P + 4) % 6]);
+    plane(k);
     PairTaps v;
-    ld2(tk + ox0, v.x[0], v.x[1]);
-    ld2(tk + oxc, v.x[2], v.x[3]);
-    ld2(tk + ox2, v.x[4], v.x[5]);
+    lds2<SK * kSlotB>(ax0, v.x[0], v.x[1]);
+    lds2<SK * kSlotB + kCtr>(ay0, v.x[2], v.x[3]);
+    lds2<SK * kSlotB>(ax2, v.x[4], v.x[5]);
+    lds2<SK * kSlotB + 0 * kRowB>(ay0, v.y[0][0], v.y[1][0]);
+    lds2<SK * kSlotB + 1 * kRowB>(ay0, v.y[0][1], v.y[1][1]);
+    v.y[0][2] = v.x[2];
+    v.y[1][2] = v.x[3];
+    lds2<SK * kSlotB + 3 * kRowB>(ay0, v.y[0][3], v.y[1][3]);
+    lds2<SK * kSlotB + 4 * kRowB>(ay0, v.y[0][4], v.y[1][4]);
 #pragma unroll
     for (int o = 0; o < 5; ++o) {
-      if (o == 2) {
-        v.y[0][2] = v.x[2];
-        v.y[1][2] = v.x[3];
-      } else {
-        ld2(tk + oy[o], v.y[0][o], v.y[1][o]);
-      }
-      v.z[0][o] = q[0][(P + o) % 5];
-      v.z[1][o] = q[1][(P + o) % 5];
+      v.z[0][o] = q[0][(P + o) % 6];
+      v.z[1][o] = q[1][(P + o) % 6];
     }
     double av[2] = {0.0, 0.0};
-    if (HAS_AUX) ld2(aring + ring_slot<kTmaRing>(k) * kPTX * kTY + 2 * t, av[0], av[1]);
+    if (HAS_AUX) lds2<SK * kAuxB>(aa, av[0], av[1]);
     body(k, (unsigned)k * pl + col, v, av, true);
   };
-  for (int k = z.k0; k < z.k1; k += 5) {
-    step(Phase<0>{}, k);
+  unsigned par = 0;
+  for (int k = z.k0; k < z.k1; k += 6, par ^= 1u) {
+    step(Phase<0>{}, k, par);
     if (k + 1 >= z.k1) break;
-    step(Phase<1>{}, k + 1);
+    step(Phase<1>{}, k + 1, par);
     if (k + 2 >= z.k1) break;
-    step(Phase<2>{}, k + 2);
+    step(Phase<2>{}, k + 2, par);
     if (k + 3 >= z.k1) break;
-    step(Phase<3>{}, k + 3);
+    step(Phase<3>{}, k + 3, par);
     if (k + 4 >= z.k1) break;
-    step(Phase<4>{}, k + 4);
+    step(Phase<4>{}, k + 4, par);
+    if (k + 5 >= z.k1) break;
+    step(Phase<5>{}, k + 5, par);
   }
-  // drain: the planes issued past the last wait (k1 .. k1+1 were waited for; later ones were never
-  // issued) -- nothing in flight remains, since issue() stops at k1 + 1
+  // nothing in flight remains: planes up to k1 + 1 were waited for, later ones were never issued
+}
+
+// F_A and/or F_D, 3-D periodic, two cells per thread on TMA-staged planes (whole 64 x 8 tiles): the
+// body of k_eval_ad3_pair (stencil3d.cuh) on walk_pair_tma, so the same operations and the same bits.
+template <bool UCONST>
+__global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_tma(Ops o, Geom g, const __grid_constant__ TmaMaps maps,
+                                                                           double* __restrict__ fa, double* __restrict__ fd,
+                                                                           int kc) {
+  extern __shared__ __align__(128) double ev_tring[];
+  const ZChunk z = zchunk(g.nz, kc);
+  const long long sbase = (long long)z.s * g.ncell;
+  double* fas = fa ? opaque(fa + sbase) : nullptr;
+  double* fds = fd ? opaque(fd + sbase) : nullptr;
+  const int s = z.s;
+  double cd[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) cd[a] = o.cdiff[s][a];
+  AdvPair<UCONST> ad;
+  ad.init(o, g);
+  walk_pair_tma<false>(
+      maps, g.nx, g.ny, g.nz, z, ev_tring, [&](int k) { ad.plane(g, k); },
+      [&](int k, unsigned cell, const PairTaps& v, const double (&)[2], bool) {
+        if (fas) {
+          double acc[2];
+          ad.acc(o, k, v, acc);
+          __stcg(reinterpret_cast<double2*>(fas + cell), make_double2(-acc[0], -acc[1]));
+          flag_wild(o.wild, wild_bits(acc[0]) | wild_bits(acc[1]));
+        }
+        if (fds) {
+          double lap[2];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            lap[c] = 0.0;
+            lap[c] = lap[c] + cd[0] * lap5(v.x[c], v.x[c + 1], v.x[c + 2], v.x[c + 3], v.x[c + 4]);
+            lap[c] = lap[c] + cd[1] * lap5(v.y[c][0], v.y[c][1], v.y[c][2], v.y[c][3], v.y[c][4]);
+            lap[c] = lap[c] + cd[2] * lap5(v.z[c][0], v.z[c][1], v.z[c][2], v.z[c][3], v.z[c][4]);
+          }
+          __stcg(reinterpret_cast<double2*>(fds + cell), make_double2(lap[0], lap[1]));
+        }
+        ad.carry_k = k + 1;
+      });
 }
 
 #ifndef __CUDACC_RTC__

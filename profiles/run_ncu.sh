@@ -26,7 +26,7 @@ if [ "${4:-hot}" = "all" ]; then
 else
   cap mg3 "k_mg3_tiled|k_mg3_pair|k_mg3_tma" 4
   cap eval k_eval_ad3 2
-  cap react "^k_react$" 2
+  cap react "^k_react$|^k_react_next$" 3
   cap rhs "^k_rhs$" 2
   cap quad "k_quad|k_mg_update|copy_unswept" 4
 fi

@@ -555,15 +555,21 @@ def test_device_looped_multigrid_cap(gpu, oracle, cap, monkeypatch):
     test_multigrid_cycle_cap_matches_oracle(gpu, oracle, cap)
 
 
-@pytest.mark.parametrize("n", [(64, 24, 33), (128, 16, 40), (64, 8, 9)])
-def test_tma_staged_multigrid_sweeps(gpu, oracle, n, monkeypatch):
-    """Whole-tile 3-D grids (nx % 64 == 0, ny % 8 == 0) run the level-0 multigrid sweeps and checks on
-    the TMA walker (tma.cuh: five bulk-tensor boxes per plane, mbarrier completion); the cp.async walker
-    is forced with CISDC_MG_TMA=0.  Both bitwise equal to the oracle (and so to each other)."""
-    spec = c5_like(n, P.constant_velocity_tables((1.0, -0.5, 0.25), n))
+@pytest.mark.parametrize("n,variable", [((64, 24, 33), False), ((128, 16, 40), False), ((64, 8, 9), False),
+                                         ((64, 16, 38), True), ((128, 8, 5), True), ((192, 24, 64), False)])
+def test_tma_staged_multigrid_sweeps(gpu, oracle, n, variable, monkeypatch):
+    """Whole-tile 3-D grids (nx % 64 == 0, ny % 8 == 0) run the level-0 multigrid sweeps and checks and
+    the F_A/F_D evaluation on the TMA walker (tma.cuh: five bulk-tensor boxes per plane, mbarrier
+    completion, plane loop unrolled by the ring size); the cp.async walkers are forced with
+    CISDC_MG_TMA=0 / CISDC_EVAL_TMA=0.  Chunk lengths of 32 planes and ragged tails (33, 38, 40, 5, 9,
+    64 planes), uniform and variable face velocities.  Both bitwise equal to the oracle (and so to
+    each other)."""
+    vel = random_velocity_tables(n) if variable else P.constant_velocity_tables((1.0, -0.5, 0.25), n)
+    spec = c5_like(n, vel)
     runs = []
     for flag in ("1", "0"):
         monkeypatch.setenv("CISDC_MG_TMA", flag)
+        monkeypatch.setenv("CISDC_EVAL_TMA", flag)
         _, g, c = per_step_compare(oracle, spec, 2, 1, workers=2)
         assert np.array_equal(g, c)
         runs.append(g)
