@@ -556,12 +556,12 @@ def test_device_looped_multigrid_cap(gpu, oracle, cap, monkeypatch):
 
 
 @pytest.mark.parametrize("n,variable", [((64, 24, 33), False), ((128, 16, 40), False), ((64, 8, 9), False),
-                                         ((64, 16, 38), True), ((128, 8, 5), True), ((192, 24, 64), False)])
+                                         ((64, 16, 38), True), ((128, 8, 13), True), ((192, 24, 64), False)])
 def test_tma_staged_multigrid_sweeps(gpu, oracle, n, variable, monkeypatch):
     """Whole-tile 3-D grids (nx % 64 == 0, ny % 8 == 0) run the level-0 multigrid sweeps and checks and
     the F_A/F_D evaluation on the TMA walker (tma.cuh: five bulk-tensor boxes per plane, mbarrier
     completion, plane loop unrolled by the ring size); the cp.async walkers are forced with
-    CISDC_MG_TMA=0 / CISDC_EVAL_TMA=0.  Chunk lengths of 32 planes and ragged tails (33, 38, 40, 5, 9,
+    CISDC_MG_TMA=0 / CISDC_EVAL_TMA=0.  Chunk lengths of 32 planes and ragged tails (33, 38, 40, 13, 9,
     64 planes), uniform and variable face velocities.  Both bitwise equal to the oracle (and so to
     each other)."""
     vel = random_velocity_tables(n) if variable else P.constant_velocity_tables((1.0, -0.5, 0.25), n)
