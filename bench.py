@@ -347,8 +347,15 @@ def main():
     f_run, f_max = clk_pre.get("sm_mhz"), clk_pre.get("sm_max_mhz")
     clock_scale = (f_run / f_max) if (f_run and f_max) else 1.0
     pk_mul_run = pk_mul.value * min(clock_scale, 1.0)
+    # CISDCQ with the fused kernel: R(m)'s Newton solve of nodes 1 .. M-1 runs inside k_react_next (class
+    # react_newton_rhs, HBM-bound: it also assembles D(m+1)'s right-hand side), node M's in the stand-alone
+    # k_react (class react_newton); the analytic Newton work is apportioned by cell solves
+    names = {c["kernel"] for c in classes}
+    newton_share = {"react_newton": 1.0}
+    if "react_newton_rhs" in names:
+        newton_share = {"react_newton": 1.0 / spec.M, "react_newton_rhs": (spec.M - 1.0) / spec.M}
     if dom["kernel"] == "react_newton" and desc.nspecies >= 9:
-        achieved = newton_flops / (dom["ms"] * 1e-3) / 1e12
+        achieved = newton_share["react_newton"] * newton_flops / (dom["ms"] * 1e-3) / 1e12
         # The kernel's arithmetic is the reference's no-FMA operation sequence (bit parity), i.e.
         # DADD / DMUL, one flop per FP64 pipe slot: its attainable peak is the measured DMUL/DADD
         # issue rate; the DFMA rate (two flops per slot) is listed beside it.
@@ -380,8 +387,9 @@ def main():
         e = {"kernel": c["kernel"], "share": c["share"], "achieved_gbs": c["gbs"], "hbm_frac": (c["gbs"] or 0) / hbm}
         if c["kernel"] in ncu:
             e["ncu"] = {k: ncu[c["kernel"]].get(k) for k in ("dram_pct", "fp64_pipe_pct", "l1_pct")}
-        if c["kernel"] == "react_newton" and desc.nspecies >= 9:
-            e["fp64_tflops"] = newton_flops / (c["ms"] * 1e-3) / 1e12
+        if c["kernel"] in newton_share and desc.nspecies >= 9:
+            e["fp64_tflops"] = newton_share[c["kernel"]] * newton_flops / (c["ms"] * 1e-3) / 1e12
+            e["fp64_work_share"] = newton_share[c["kernel"]]
             e["fp64_frac_dmul_dadd_peak"] = e["fp64_tflops"] / pk_mul_run
             e["fp64_frac_peak_after_run"] = e["fp64_tflops"] / pk_mul_s.value
             e["fp64_frac_burst_peak"] = e["fp64_tflops"] / pk_mul.value

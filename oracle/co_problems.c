@@ -228,7 +228,10 @@ void co_problem_destroy(co_problem* p) {
 }
 
 size_t co_problem_dim(const co_problem* p) { return p->dim; }
-int co_problem_has_coupled(const co_problem* p) { return p->d.kind == CISDC_PROBLEM_LINEAR_SCALAR; }
+int co_problem_has_coupled(const co_problem* p) {
+  return p->d.kind == CISDC_PROBLEM_LINEAR_SCALAR ||
+         (p->d.kind == CISDC_PROBLEM_PERIODIC_ADR && p->d.coupled_max_iter > 0);
+}
 const char* co_problem_error(const co_problem* p) { return p->err; }
 
 /* ------------------------------------------------------------------ periodic ADR operators */
@@ -1127,6 +1130,64 @@ static int rd_solve_reaction(co_problem* p, double coef, const double* rhs, doub
   return CISDC_OK;
 }
 
+/* ------------------------------------------------------------------ coupled D+R stage (periodic ADR)
+ *
+ * OperatorSplitProblem::solve_coupled (operator_split.hpp:49-53): phi - coef (F_D(phi) + F_R(phi)) = rhs.
+ * The reference PDE class provides none; the periodic ADR class defines it (cisdc_gpu.h, "coupled
+ * stage") as the fixed point of the alternating diffusion / reaction stage solves -- the nested
+ * iteration of cisdcq_cells at one node (integrators.cpp:195-258), whose limit is the coupled solve
+ * (test_integrators.cpp:195-213) -- run to convergence:
+ *   y_0 = rhs;  z = solve_D(coef, rhs + coef F_R(y_k));  y_{k+1} = solve_R(coef, rhs + coef F_D(z));
+ *   stop when max|y_{k+1} - y_k| <= coupled_tol * max|y_{k+1}|; SolveError after coupled_max_iter. */
+static int adr_solve_diffusion_any(co_problem* p, double coef, const double* rhs, double* out, cisdc_counters* c) {
+  if (p->d.diffusion_solver == CISDC_DIFFUSION_DIRECT) return adr_solve_diffusion_scan(p, coef, rhs, out);
+  if (p->d.diffusion_solver == CISDC_DIFFUSION_BANDED_ORACLE) return adr_solve_diffusion_direct(p, coef, rhs, out);
+  return adr_solve_diffusion_mg(p, coef, rhs, out, c);
+}
+
+static int adr_solve_coupled(co_problem* p, double coef, const double* rhs, double* out, cisdc_counters* c) {
+  const size_t n = p->dim;
+  if (coef == 0.0) {
+    memmove(out, rhs, sizeof(double) * n);
+    return CISDC_OK;
+  }
+  double* y = (double*)malloc(sizeof(double) * n);
+  double* f = (double*)malloc(sizeof(double) * n);
+  double* b = (double*)malloc(sizeof(double) * n);
+  double* z = (double*)malloc(sizeof(double) * n);
+  double* yn = (double*)malloc(sizeof(double) * n);
+  int rc = CISDC_OK, converged = 0;
+  memcpy(y, rhs, sizeof(double) * n);
+  for (int it = 0; it < p->d.coupled_max_iter && !converged; ++it) {
+    adr_reaction(p, y, f);
+    for (size_t i = 0; i < n; ++i) b[i] = rhs[i] + coef * f[i];
+    rc = adr_solve_diffusion_any(p, coef, b, z, c);
+    if (rc) break;
+    adr_diffusion(p, z, f);
+    for (size_t i = 0; i < n; ++i) b[i] = rhs[i] + coef * f[i];
+    rc = adr_solve_reaction(p, coef, b, yn, c);
+    if (rc) break;
+    double delta = 0.0, scale = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      const double d = fabs(yn[i] - y[i]), a = fabs(yn[i]);
+      if (d > delta) delta = d;
+      if (a > scale) scale = a;
+    }
+    double* t = y;
+    y = yn;
+    yn = t;
+    converged = delta <= p->d.coupled_tol * scale;
+  }
+  if (!rc && !converged) rc = fail(p, CISDC_E_SOLVE, "periodic ADR: coupled solve did not converge");
+  if (!rc) memcpy(out, y, sizeof(double) * n);
+  free(y);
+  free(f);
+  free(b);
+  free(z);
+  free(yn);
+  return rc;
+}
+
 /* ------------------------------------------------------------------ dispatch */
 
 int co_eval(co_problem* p, int stage, const double* phi, double* out) {
@@ -1176,6 +1237,7 @@ int co_solve(co_problem* p, int stage, double coef, const double* rhs, double* o
         return adr_solve_diffusion_mg(p, coef, rhs, out, c);
       }
       if (stage == CISDC_STAGE_REACTION) return adr_solve_reaction(p, coef, rhs, out, c);
+      if (p->d.coupled_max_iter > 0) return adr_solve_coupled(p, coef, rhs, out, c);
       return fail(p, CISDC_E_CAPABILITY, "OperatorSplitProblem: coupled diffusion-reaction solve not provided");
   }
 }

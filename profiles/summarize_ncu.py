@@ -11,7 +11,7 @@ import os
 import sys
 
 # kernel base name -> bench.py kernel class
-CLASS = {"k_react": "react_newton", "k_react_next": "react_newton_rhs", "k_eval_ad3_tiled": "eval_ad", "k_eval_ad3_pair": "eval_ad",
+CLASS = {"k_react": "react_newton", "k_react_next": "react_newton_rhs", "k_eval_ad3_tiled": "eval_ad", "k_eval_ad3_pair": "eval_ad", "k_eval_ad3_tma": "eval_ad",
          "k_eval_ad2_rows": "eval_ad", "k_rhs": "rhs", "k_quad_base": "quad_base", "k_mg3_tiled": "mg_smooth",
          "k_mg3_pair": "mg_smooth", "k_mg3_tma": "mg_smooth", "k_mg2_rows": "mg_smooth", "k_mg_update": "mg_norm",
          "k_mg_copy_unswept": "mg_norm"}
