@@ -117,6 +117,17 @@ typedef struct cisdc_problem_desc {
   double mg_omega;          /* weighted-Jacobi damping */
   /* CISDC_PROBLEM_REFERENCE_RD / LINEAR_SCALAR coefficients (a, d, r); n[0] = n_x for RD */
   double ref_a, ref_d, ref_r;
+  /* Coupled stage of the periodic ADR class (OperatorSplitProblem::solve_coupled,
+   * operator_split.hpp:49-53; imexq_sweep's stage solve, integrators.cpp:166):
+   *   phi - coef (F_D(phi) + F_R(phi)) = rhs
+   * as the fixed point of the alternating stage solves (the nested iteration of cisdcq_cells at one
+   * node, integrators.cpp:195-258, run to convergence):
+   *   y_0 = rhs;  z = solve_diffusion(coef, rhs + coef F_R(y_k));  y_{k+1} = solve_reaction(coef, rhs + coef F_D(z))
+   * until max|y_{k+1} - y_k| <= coupled_tol * max|y_{k+1}|; SolveError after coupled_max_iter
+   * iterations.  coupled_max_iter == 0: no coupled solve (has_coupled_solve() == false, imexq_sweep
+   * raises CapabilityError, as for the reference's ReactionDiffusionProblem). */
+  double coupled_tol;
+  int coupled_max_iter;
 } cisdc_problem_desc;
 
 /* cisdc::QuadratureTables, row-major, M <= CISDC_MAX_M (proj/core/include/cisdc/quadrature.hpp:47-60) */

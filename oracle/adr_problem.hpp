@@ -45,6 +45,17 @@ class AdrProblem final : public cisdc::OperatorSplitProblem {
   void solve_reaction(double coef, std::span<const double> b, std::span<double> o) const override {
     sv(CISDC_STAGE_REACTION, coef, b, o);
   }
+  // the periodic ADR class's coupled stage (cisdc_gpu.h: alternating stage solves to convergence);
+  // it runs diffusion solves inside, so it takes the multigrid-workspace lock as well
+  bool has_coupled_solve() const override { return co_problem_has_coupled(p_) != 0; }
+  void solve_coupled(double coef, std::span<const double> b, std::span<double> o) const override {
+    if (!co_problem_has_coupled(p_)) {
+      cisdc::OperatorSplitProblem::solve_coupled(coef, b, o);
+      return;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    sv(3, coef, b, o);
+  }
   long long newton() const { return newton_.load(); }
   long long mg() const { return mg_.load(); }
   void reset() {

@@ -48,6 +48,8 @@ class ProblemDescC(C.Structure):
         ("ref_a", C.c_double),
         ("ref_d", C.c_double),
         ("ref_r", C.c_double),
+        ("coupled_tol", C.c_double),
+        ("coupled_max_iter", C.c_int),
     ]
 
 

@@ -138,6 +138,11 @@ struct cisdc_gpu_ctx {
   double* fd_ad[kMaxM + 1] = {};
   std::vector<double*> slot_bufs;  // (nu-1) * M * 5: phi_ad, phi_r, fa_r, fd_r, fr_r
   std::vector<double*> diff_bufs;  // CISDCQ rhs difference cache: (M - 3) nodes x {dA, dDR}
+  // coupled stage of the periodic ADR class (allocated on first use): y, y_next, f / stage rhs, z;
+  // the convergence maxima on the device and their pinned mirror (delta, scale, fail_key)
+  double* cpl[4] = {};
+  unsigned long long* d_cpl = nullptr;
+  unsigned long long* h_cpl = nullptr;
   // solvers
   double* rd_work = nullptr;
   MgHierarchy mg;
@@ -703,6 +708,74 @@ int check_status(cisdc_gpu_ctx* ctx, cisdc_counters* counters) {
   return CISDC_OK;
 }
 
+// ---------------------------------------------------------------- coupled stage (periodic ADR)
+
+bool has_coupled(const cisdc_gpu_ctx* ctx) {
+  return ctx->linear || (!ctx->ref_rd && ctx->desc.coupled_max_iter > 0);
+}
+
+// OperatorSplitProblem::solve_coupled (operator_split.hpp:49-53) of the periodic ADR class, as
+// cisdc_gpu.h defines it: y_0 = rhs; z = solve_D(coef, rhs + coef F_R(y_k)); y_{k+1} =
+// solve_R(coef, rhs + coef F_D(z)) until max|y_{k+1} - y_k| <= coupled_tol max|y_{k+1}|.  Every step is
+// one of the engine's stage kernels (F_R, the multigrid or 1-D direct solve, F_D, the Newton
+// kernel); the host reads the two maxima (exact, so bit-equal to the oracle's serial loop) and the
+// failure word once per iteration.  A stage failure inside ends the iteration and is reported by
+// check_status with the failing stage's message, as the oracle returns it.
+int solve_coupled_adr(cisdc_gpu_ctx* ctx, double coef, const double* rhs, double* out, cudaStream_t s,
+                      cisdc_counters* c) {
+  const long long n = ctx->g.n;
+  if (coef == 0.0) {
+    if (out != rhs) CU(cudaMemcpyAsync(out, rhs, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    return CISDC_OK;
+  }
+  if (!ctx->cpl[0]) {
+    for (int b = 0; b < 4; ++b) TRY(dalloc(ctx, &ctx->cpl[b], n));
+    double* d2 = nullptr;
+    TRY(dalloc(ctx, &d2, 2));
+    ctx->d_cpl = reinterpret_cast<unsigned long long*>(d2);
+    CU(cudaMallocHost(&ctx->h_cpl, 3 * sizeof(unsigned long long)));
+  }
+  double *y = ctx->cpl[0], *yn = ctx->cpl[1], *f = ctx->cpl[2], *z = ctx->cpl[3];
+  const double* cur = rhs;  // y_0 = rhs, read in place
+  const int blocks = grid_of(n, 256);
+  bool converged = false;
+  for (int it = 0; it < ctx->desc.coupled_max_iter && !converged; ++it) {
+    TRY(launch_eval_r(ctx, cur, f, s));
+    ctx->tm.before(kKRhs, s);
+    k_axpy_inplace<<<blocks, 256, 0, s>>>(rhs, coef, f, n);
+    ctx->tm.after(kKRhs, s, 3.0 * F8(ctx));
+    TRY(solve_diffusion(ctx, coef, f, z, s));
+    TRY(launch_eval_ad(ctx, z, nullptr, f, s));
+    ctx->tm.before(kKRhs, s);
+    k_axpy_inplace<<<blocks, 256, 0, s>>>(rhs, coef, f, n);
+    ctx->tm.after(kKRhs, s, 3.0 * F8(ctx));
+    ReactArgs a{};
+    a.coef = coef;
+    a.p0 = f;
+    a.phi_out = yn;
+    a.fr_out = nullptr;
+    TRY(launch_react(ctx, kModePlain, a, s));
+    CU(cudaMemsetAsync(ctx->d_cpl, 0, 2 * sizeof(unsigned long long), s));
+    ctx->tm.before(kKIncr, s);
+    k_coupled_delta<<<std::min(blocks, 8 * ctx->num_sms), 256, 0, s>>>(yn, cur, n, ctx->d_cpl);
+    ctx->tm.after(kKIncr, s, 2.0 * F8(ctx));
+    CU(cudaGetLastError());
+    CU(cudaMemcpyAsync(ctx->h_cpl, ctx->d_cpl, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(ctx->h_cpl + 2, &ctx->d_st->fail_key, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    if (ctx->h_cpl[2] != ~0ull) return check_status(ctx, c);  // a stage solve inside failed
+    double delta, scale;
+    std::memcpy(&delta, ctx->h_cpl, sizeof(double));
+    std::memcpy(&scale, ctx->h_cpl + 1, sizeof(double));
+    converged = delta <= ctx->desc.coupled_tol * scale;
+    std::swap(y, yn);  // the new iterate is y
+    cur = y;
+  }
+  if (!converged) return set_err(ctx, CISDC_E_SOLVE, "periodic ADR: coupled solve did not converge");
+  CU(cudaMemcpyAsync(out, cur, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  return CISDC_OK;
+}
+
 // ---------------------------------------------------------------- sweeps
 
 double QI(const cisdc_tables& t, int m, int j) { return t.QtI[m * t.M + j]; }
@@ -780,7 +853,7 @@ int sweep_misdcq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
 // phi_AD = phi, and the three evaluations at phi.  Only problems with a coupled solve (the
 // linear scalar model, as in the reference) run it.
 int sweep_imexq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
-  if (!ctx->linear)
+  if (!has_coupled(ctx))
     return set_err(ctx, CISDC_E_CAPABILITY, "imexq_sweep: problem provides no coupled diffusion-reaction solve");
   const int M = ctx->M, prev = ctx->cur, nxt = 1 - ctx->cur;
   cudaStream_t s = ctx->s_main;
@@ -810,7 +883,8 @@ int sweep_imexq(cisdc_gpu_ctx* ctx, double dt, cisdc_counters* c) {
     r.out = ctx->rhs_d;
     TRY(launch_rhs(ctx, r, s));
     double* phi = ctx->own[nxt][kPhi][m + 1];
-    TRY(linear_solve(ctx, CISDC_STAGE_COUPLED, coef, ctx->rhs_d, phi, s));
+    if (ctx->linear) TRY(linear_solve(ctx, CISDC_STAGE_COUPLED, coef, ctx->rhs_d, phi, s));
+    else TRY(solve_coupled_adr(ctx, coef, ctx->rhs_d, phi, s, c));
     if (c) ++c->coupled;
     CU(cudaMemcpyAsync(ctx->phi_ad[m + 1], phi, sizeof(double) * ctx->g.n, cudaMemcpyDeviceToDevice, s));
     TRY(launch_eval_ad(ctx, phi, ctx->own[nxt][kFa][m + 1], ctx->own[nxt][kFd][m + 1], s));
@@ -1183,6 +1257,7 @@ void cisdc_gpu_destroy(cisdc_gpu_ctx* ctx) {
   mg_free(ctx->mg);
   rtc_free(ctx->rtc);
   if (ctx->h_st) cudaFreeHost(ctx->h_st);
+  if (ctx->h_cpl) cudaFreeHost(ctx->h_cpl);
   if (ctx->h_incr) cudaFreeHost(ctx->h_incr);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : ctx->trace_ev) cudaEventDestroy(e);
@@ -1528,6 +1603,8 @@ int cisdc_gpu_solve(cisdc_gpu_ctx* ctx, int stage, double coef, const double* rh
     TRY(launch_react(ctx, kModePlain, a, s));
   } else if (ctx->linear) {
     TRY(linear_solve(ctx, CISDC_STAGE_COUPLED, coef, ctx->rhs_d, ctx->scratch, s));
+  } else if (has_coupled(ctx)) {
+    TRY(solve_coupled_adr(ctx, coef, ctx->rhs_d, ctx->scratch, s, inout));
   } else {
     return set_err(ctx, CISDC_E_CAPABILITY, "OperatorSplitProblem: coupled diffusion-reaction solve not provided");
   }
@@ -1557,7 +1634,8 @@ static bool step_graph_ok(const cisdc_gpu_ctx* ctx, const cisdc_integrate_option
   const char* e = std::getenv("CISDC_STEP_GRAPH");
   if (e && e[0] == '0') return false;
   const bool host_mg = !ctx->ref_rd && !ctx->linear && ctx->desc.diffusion_solver == CISDC_DIFFUSION_MULTIGRID;
-  return !o->has_stop_tol && !ctx->tm.on && !ctx->trace_on && !host_mg;
+  const bool host_coupled = o->scheme == CISDC_SCHEME_IMEXQ && !ctx->linear;  // the host reads every iteration's maxima
+  return !o->has_stop_tol && !ctx->tm.on && !ctx->trace_on && !host_mg && !host_coupled;
 }
 
 static cisdc_gpu_ctx::StepGraph* find_step_graph(cisdc_gpu_ctx* ctx, const cisdc_integrate_options* o) {

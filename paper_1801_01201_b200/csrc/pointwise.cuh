@@ -158,6 +158,34 @@ __global__ void __launch_bounds__(256) k_lin_div(const double* __restrict__ rhs,
   if (e < n) out[e] = rhs[e] / denom;
 }
 
+// Coupled stage of the periodic ADR class (cisdc_gpu.h): f <- rhs + coef * f, the stage right-hand
+// side of the alternating iteration (no contraction: the oracle's a + c * b is a product, then a sum)
+__global__ void __launch_bounds__(256) k_axpy_inplace(const double* __restrict__ rhs, double coef, double* __restrict__ f,
+                                                      long long n) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) f[e] = __dadd_rn(rhs[e], __dmul_rn(coef, f[e]));
+}
+// out2[0] = max |yn - y|, out2[1] = max |yn| as the bit patterns of non-negative doubles (ordered like
+// the values; maxima are exact, so the order of the reduction does not matter).  out2 zeroed before.
+__global__ void __launch_bounds__(256) k_coupled_delta(const double* __restrict__ yn, const double* __restrict__ y,
+                                                       long long n, unsigned long long* __restrict__ out2) {
+  double d = 0.0, a = 0.0;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const double v = yn[e];
+    d = fmax(d, fabs(v - y[e]));
+    a = fmax(a, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+    a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out2, (unsigned long long)__double_as_longlong(d));
+    atomicMax(out2 + 1, (unsigned long long)__double_as_longlong(a));
+  }
+}
+
 constexpr int kIncrBlocks = 1184;  // 8 x 148 SMs; fixed so the reduction tree is fixed
 constexpr int kIncrThreads = 256;
 static_assert(kIncrBlocks <= 2048, "k_incr_final folds at most two partials per thread");

@@ -64,6 +64,8 @@ class ProblemDesc:
     ref_a: float = 0.0
     ref_d: float = 0.0
     ref_r: float = 0.0
+    coupled_tol: float = 1e-13     # periodic ADR coupled stage (cisdc_gpu.h); used when coupled_max_iter > 0
+    coupled_max_iter: int = 0      # 0: no coupled solve (IMEXQ raises CapabilityError, like the reference PDE)
     name: str = ""
 
     @property
@@ -118,6 +120,8 @@ class ProblemDesc:
         d.mg_min_coarse = self.mg_min_coarse
         d.mg_omega = self.mg_omega
         d.ref_a, d.ref_d, d.ref_r = self.ref_a, self.ref_d, self.ref_r
+        d.coupled_tol = self.coupled_tol
+        d.coupled_max_iter = self.coupled_max_iter
         return d
 
 

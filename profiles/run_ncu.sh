@@ -14,7 +14,7 @@ STEP="python tools/profile_step.py --config $CFG --scale $SCALE"
 $N --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_${CFG}.csv $STEP > gpurun_out/ncu_${TAG}_l.log 2>&1
 cap() {  # name regex count
   local rep=/tmp/${TAG}_${CFG}_$1
-  $N --set full --clock-control none --cache-control ${CACHE:-all} --import-source on -k "regex:$2" -c $3 -f -o $rep $STEP > gpurun_out/ncu_${TAG}_$1.log 2>&1
+  $N --set full --clock-control none --cache-control ${CACHE:-all} --import-source on -k "regex:$2" -s ${SKIP:-0} -c $3 -f -o $rep $STEP > gpurun_out/ncu_${TAG}_$1.log 2>&1
   $N -i $rep.ncu-rep --page raw --csv > gpurun_out/${TAG}_${CFG}_$1_raw.csv 2>/dev/null
   $N -i $rep.ncu-rep --page details --csv > gpurun_out/${TAG}_${CFG}_$1_details.csv 2>/dev/null
   $N -i $rep.ncu-rep --page source --csv --print-source sass > gpurun_out/${TAG}_${CFG}_$1_source.csv 2>/dev/null
@@ -26,7 +26,8 @@ if [ "${4:-hot}" = "all" ]; then
 else
   cap mg3 "k_mg3_tiled|k_mg3_pair|k_mg3_tma" 4
   cap eval k_eval_ad3 2
-  cap react "^k_react$|^k_react_next$" 3
+  # the second sweep's Newton launches (the first sweep's fields alias node 0): D(2..M)'s rhs rows
+  SKIP=6 cap react "^k_react$|^k_react_next$" 6
   cap rhs "^k_rhs$" 2
   cap quad "k_quad|k_mg_update|copy_unswept" 4
 fi

@@ -87,6 +87,7 @@ def main():
             lines.append(f"| {k} | {n} | {us / 1e3:.2f} | {us / n:.1f} | {100 * us / tot:.1f}% |")
         lines += [f"| **total** | | **{tot / 1e3:.2f}** | | |", ""]
     traffic = {}
+    acc = {}
     lines += ["## `--set full` captures", "", "| kernel | " + " | ".join(n for _, n in METRICS) + " | DRAM GB/s |",
               "|---|" + "---:|" * (len(METRICS) + 1)]
     for part in ("react", "eval", "mg3", "rhs", "quad", "rhsd", "all"):
@@ -117,12 +118,21 @@ def main():
             name = r["kernel"].split("(")[0].replace("void ", "")
             lines.append(f"| {name} | " + " | ".join(cells) + f" | {gbs:.0f} |")
             cls = CLASS.get(base_name(r["kernel"]))
-            if cls and cls not in traffic:
-                traffic[cls] = {"kernel": name, "dram_bytes": rd + wr, "time_us": t,
-                                "dram_pct": r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
-                                "fp64_pipe_pct": r.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
-                                "l1_pct": r.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
-                                "source": f"profiles/{tag[:2]}/{tag}_{cfg}_{part}_raw.csv.gz (first captured launch)"}
+            if cls:
+                acc.setdefault(cls, []).append({
+                    "kernel": name, "dram_bytes": rd + wr, "time_us": t,
+                    "dram_pct": r.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                    "fp64_pipe_pct": r.get("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "l1_pct": r.get("l1tex__throughput.avg.pct_of_peak_sustained_active"),
+                    "part": part})
+    # per class: the mean over the captured launches (bench.py's `achieved` is a per-launch mean too)
+    for cls, rows in acc.items():
+        n = len(rows)
+        mean = {k: sum((r[k] or 0.0) for r in rows) / n for k in ("dram_bytes", "time_us", "dram_pct", "fp64_pipe_pct", "l1_pct")}
+        mean["kernel"] = rows[0]["kernel"]
+        mean["launches_captured"] = n
+        mean["source"] = f"profiles/{tag[:2]}/{tag}_{cfg}_{rows[0]['part']}_raw.csv.gz (mean of {n} captured launch(es))"
+        traffic[cls] = mean
     lines.append("")
     name = f"{tag}_summary.md" if cfg == "c5" else f"{tag}_{cfg}_summary.md"
     with open(os.path.join(here, name), "w") as f:

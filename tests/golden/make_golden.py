@@ -9,6 +9,9 @@ against them without needing /root/reference.
                   dt = 0.05, M = 4, 3 steps x 4 sweeps): misdc, misdcq, cisdcq nu = 1/3, both conventions
   periodic.npz    the reference integrators driving the periodic ADR problem class (configs 1-5 at
                   reduced size): final state, increments, solve / Newton / multigrid counts
+  imexq_adr.npz   (--imexq writes only this one) the reference's imexq_sweep driving the periodic ADR class's
+                  coupled stage (configs 1, 2, 3, 5 at reduced size): final state, increments, per-step
+                  sweeps / coupled solves / Newton trips / multigrid cycles
   full_<cfg>.json (--full [c3 c4 c5]) the same at the BASELINE configs' FULL sizes, one time step:
                   C3 1024^2 x 3 (misdc, misdcq, cisdcq), C4 2048^2 x 9 (misdc, misdcq, cisdcq),
                   C5 256^3 x 9 (cisdcq nu = 1 through execute_pipelined, the bench workload).  The
@@ -59,6 +62,39 @@ FULL = {
     "c4": (lambda: P.config_c4(n_steps=1), (0, 1, 2)),
     "c5": (lambda: P.config_c5(n_steps=1), (2,)),
 }
+
+
+# IMEXQ on the periodic ADR class (its coupled stage, cisdc_gpu.h): the unmodified imexq_sweep
+# (integrators.cpp:145-173) driving AdrProblem::solve_coupled; (config, M, sweeps, steps)
+IMEXQ_ADR = {
+    "c1": (lambda: P.config_c1(scale=4), 3, 3, 2),
+    "c2": (lambda: P.config_c2(scale=128, n_steps=2), 3, 3, 2),
+    "c3": (lambda: P.config_c3(scale=32, n_steps=1), 3, 2, 1),
+    "c5": (lambda: P.config_c5(scale=32), 2, 2, 1),
+}
+
+
+def imexq_adr_case(name):
+    import dataclasses
+    make, M, sweeps, steps = IMEXQ_ADR[name]
+    spec = make()
+    prob = dataclasses.replace(spec.problem, coupled_tol=1e-13, coupled_max_iter=60)
+    o = api.IntegrateOptions(scheme=3, dt=spec.dt, n_steps=steps, M=M, n_sweeps=sweeps, nu=1)
+    return spec, prob, o
+
+
+def imexq_adr():
+    out = {}
+    for name in IMEXQ_ADR:
+        spec, prob, o = imexq_adr_case(name)
+        f, reps, incs = O.ref_integrate(prob, spec.phi0, o)
+        out[f"{name}_phi0"] = spec.phi0
+        out[f"{name}_final"] = f
+        out[f"{name}_incs"] = incs
+        out[f"{name}_counts"] = np.array([[r.sweeps, r.counters.coupled, r.counters.newton_iterations,
+                                           r.counters.mg_cycles] for r in reps])
+        print("imexq", name, prob.n, out[f"{name}_counts"].tolist(), flush=True)
+    np.savez_compressed(os.path.join(HERE, "imexq_adr.npz"), **out)
 
 
 def sha(a: np.ndarray) -> str:
@@ -115,6 +151,9 @@ def main():
         return
     if O.ref_lib() is None:
         raise SystemExit("oracle/_ref not available: build it with make -C oracle ref (needs /root/reference)")
+    if len(sys.argv) > 1 and sys.argv[1] == "--imexq":
+        imexq_adr()
+        return
     out = {}
     for M in range(1, 9):
         for conv in (0, 1):
@@ -148,6 +187,7 @@ def main():
             per[k + "_counts"] = np.array([reps[0].counters.newton_iterations, reps[0].counters.mg_cycles] +
                                           [r.sweeps for r in reps])
     np.savez_compressed(os.path.join(HERE, "periodic.npz"), **per)
+    imexq_adr()
     print("golden fixtures written to", HERE)
 
 
