@@ -174,7 +174,7 @@ def workload_config(cfg_name: str, spec, scheme: int, workers: int) -> dict:
     n = list(desc.n[: desc.ndim])
     dofs = int(np.prod(n)) * desc.nspecies
     return {"workload": f"{cfg_name}: {desc.name} {'x'.join(map(str, n))} x {desc.nspecies} species",
-            "scheme": ["misdc", "misdcq", "cisdcq"][scheme], "nu": spec.nu, "workers": workers, "M": spec.M,
+            "scheme": ["misdc", "misdcq", "cisdcq", "imexq"][scheme], "nu": spec.nu, "workers": workers, "M": spec.M,
             "sweeps_per_step": spec.n_sweeps, "dt": spec.dt, "dofs": dofs, "updates_per_step": dofs * spec.M * spec.n_sweeps,
             "l2": ("inputs larger than L2 (each field %.2f GB)" if 8 * dofs > 126e6 else
                    "fields fit in L2 (each field %.4f GB; no flush: the configuration itself is that small)")
@@ -240,6 +240,9 @@ def main():
     scheme = spec.scheme if args.scheme is None else args.scheme
     workers = args.workers if scheme == 2 else 0
     desc = spec.problem
+    if scheme == 3:  # IMEXQ: the periodic ADR class's coupled stage (cisdc_gpu.h), the paper's baseline scheme
+        import dataclasses
+        desc = dataclasses.replace(desc, coupled_tol=1e-13, coupled_max_iter=60)
     n = desc.dim
     ctx = api.GpuContext(desc, spec.M, spec.convention)
     opt = api.IntegrateOptions(scheme=scheme, dt=spec.dt, n_steps=1, M=spec.M, n_sweeps=spec.n_sweeps, nu=spec.nu,

@@ -330,7 +330,7 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
 template <int S>
 int launch_eval_r_s(cisdc_gpu_ctx* ctx, const double* phi, double* fr, cudaStream_t s) {
   ctx->tm.before(kKEvalR, s);
-  k_eval_r<S><<<grid_of(ctx->g.ncell, 128), 128, 0, s>>>(ctx->rx, ctx->g, phi, fr);
+  k_eval_r<S><<<grid_of(ctx->g.ncell, 128), 128, 0, s>>>(ctx->rx, ctx->g, phi, fr, ctx->ops.wild);
   ctx->tm.after(kKEvalR, s, 2.0 * F8(ctx));
   CU(cudaGetLastError());
   return CISDC_OK;
@@ -480,7 +480,8 @@ double rhs_fields(const RhsArgs& a) {
       else in.insert(in.end(), {T.D, T.Dp, T.R, T.Rp});
     }
   }
-  in.insert(in.end(), {a.X, a.Y, a.Z});
+  if (a.kind == kRhsCisdcq && a.X == a.Y) in.push_back(a.Z);  // X - Y = +0.0: X is not read (rhs.cuh)
+  else in.insert(in.end(), {a.X, a.Y, a.Z});
   double outs = 1 + (a.out2 != nullptr) + (a.base_out != nullptr);
   for (int t = 0; t < a.nt; ++t) outs += (a.t[t].outA != nullptr) + (a.t[t].outDR != nullptr);
   return distinct_fields(in) + outs;

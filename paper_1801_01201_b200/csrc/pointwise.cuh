@@ -132,7 +132,8 @@ __global__ void __launch_bounds__(256) k_rhs(const __grid_constant__ RhsArgs a, 
       r += T.cE * dA + tI;
     }
   }
-  r += a.fc * (a.X[e] - a.Y[e]) - a.fc * a.Z[e];
+  if (rhs_same_xy(a, tame)) r += a.fc * 0.0 - a.fc * a.Z[e];  // X - Y = +0.0 exactly (rhs.cuh)
+  else r += a.fc * (a.X[e] - a.Y[e]) - a.fc * a.Z[e];
   a.out[e] = r;
 }
 

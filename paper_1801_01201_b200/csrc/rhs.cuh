@@ -54,6 +54,13 @@ struct RhsArgs {
   const int* wild;  // Ops::wild of the context
 };
 
+// kRhsCisdcq's lagged-reaction term fc * (X - Y): for ell == 1 (always, when nu == 1) X and Y are the
+// SAME field, F_R of the previous sweep at this node (integrators.cpp:222-224 with fr_lag == fr_p).
+// For a finite value x - x is +0.0 exactly, so the term is fc * 0.0 (a zero with fc's sign) and X is
+// not read: one field less per launch.  Every F_R store flags non-finite values in Ops::wild as well
+// (newton.cuh react_finish, k_eval_r); once flagged, X - Y is evaluated as written (Inf - Inf = NaN).
+__device__ __forceinline__ bool rhs_same_xy(const RhsArgs& a, bool tame) { return tame && a.X == a.Y; }
+
 // cE * (A - Ap) + tI with the skipA shortcut above
 __device__ __forceinline__ double rhs_term_a(const RhsTerm& T, long long e, double tI, bool skip) {
   if (skip && tI != 0.0) return tI;
@@ -123,6 +130,16 @@ __device__ __forceinline__ void rhs_cisdcq_cell(const RhsArgs& a, long long c, l
     }
   }
   double x[S], y[S], z[S];
+  if (rhs_same_xy(a, tame)) {  // X - Y = +0.0 exactly: X is not read (header comment)
+#pragma unroll
+    for (int s = 0; s < S; ++s) z[s] = a.Z[(long long)s * ncell + c];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      r[s] += a.fc * 0.0 - a.fc * z[s];
+      a.out[(long long)s * ncell + c] = r[s];
+    }
+    return;
+  }
 #pragma unroll
   for (int s = 0; s < S; ++s) {
     const long long e = (long long)s * ncell + c;

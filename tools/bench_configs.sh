@@ -28,3 +28,5 @@ run c1_misdc --config c1 --scheme 0 --steps 20 --warmup 5
 run c2_misdc --config c2 --scheme 0 --steps 10 --warmup 3
 run c3_misdc --config c3 --scheme 0 --steps 5 --warmup 3
 run c4_misdc --config c4 --scheme 0 --steps 5 --warmup 3
+run c5_imexq --config c5 --scheme 3 --steps 2 --warmup 1
+run c3_imexq --config c3 --scheme 3 --steps 2 --warmup 1
