@@ -299,12 +299,11 @@ int launch_eval_ad(cisdc_gpu_ctx* ctx, const double* phi, double* fa, double* fd
           tma_maps(maps, phi, nullptr, g.nx, g.ny, g.nz * g.S)) {
         CU(func_attr_once(k_eval_ad3_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaEvalSmem));
         CU(func_attr_once(k_eval_ad3_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaEvalSmem));
+        const dim3 eg = tile3d_pair_grid(g.nx, g.ny, g.nz, g.S);
         if (ctx->ops.vconst)
-          k_eval_ad3_tma<true><<<tile3d_pair_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), kTmaEvalSmem, s>>>(
-              ctx->ops, g, maps, fa, fd, kZChunk);
+          k_eval_ad3_tma<true><<<eg, dim3(kTX, kTY), kTmaEvalSmem, s>>>(ctx->ops, g, maps, fa, fd, kZChunk);
         else
-          k_eval_ad3_tma<false><<<tile3d_pair_grid(g.nx, g.ny, g.nz, g.S), dim3(kTX, kTY), kTmaEvalSmem, s>>>(
-              ctx->ops, g, maps, fa, fd, kZChunk);
+          k_eval_ad3_tma<false><<<eg, dim3(kTX, kTY), kTmaEvalSmem, s>>>(ctx->ops, g, maps, fa, fd, kZChunk);
       } else if (g.nx % 2 == 0 && eval_pair()) {
         CU(func_attr_once(k_eval_ad3_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));
         CU(func_attr_once(k_eval_ad3_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPairSmem));

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kTX* kTY, 3) k_mg3_tma(const __grid_constant__
   const int s = z.s;
   const double cs0 = C.c[s][0], cs1 = C.c[s][1], cs2 = C.c[s][2], coef = C.coef, wd = C.wD[s];
   double m = 0.0, mb = 0.0;
-  walk_pair_tma<!BMAX>(maps, nx, ny, nz, z, mg_tring, [](int) {},
+  walk_pair_tma<!BMAX, false>(maps, nx, ny, nz, z, mg_tring, [](int) {},
                                     [&](int, unsigned cell, const PairTaps& v, const double (&bva)[2], bool) {
                                       double xn[2];
                                       const double bv[2] = {BMAX ? v.x[2] : bva[0], BMAX ? v.x[3] : bva[1]};

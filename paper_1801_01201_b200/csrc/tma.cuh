@@ -10,7 +10,8 @@
 // wrapped origin, so no box ever crosses a seam and nothing is zero-filled.  The right-hand side
 // rides in the same transaction (one 64 x 8 box).  Completion is an mbarrier per ring slot
 // (arrive.expect_tx by the producer, complete_tx by the copies, try_wait.parity by all threads);
-// the per-plane __syncthreads of the walker stays as the slot-reuse (WAR) fence.
+// slot reuse (WAR) is fenced by the walker's per-plane __syncthreads (multigrid sweeps) or by a second
+// "empty" mbarrier per slot (F_A/F_D: FREE, below).
 //
 // Shared-memory plane slot (doubles; every region 128-byte aligned, as the bulk tensor copy needs;
 // rows -2 .. 9 are contiguous at pitch 64, so a thread's five y taps and its centre are one base
@@ -39,8 +40,8 @@ constexpr int kTmaSlot = 800;                               // doubles per plane
 constexpr unsigned kTmaPlaneBytes = kTmaSlot * 8u;          // 6400 bytes of x per plane
 constexpr unsigned kTmaAuxBytes = kPTX * kTY * 8u;          // 4096 bytes of rhs per plane
 constexpr int kTmaRing = 6;
-constexpr size_t kTmaSmem = (size_t)kTmaRing * (kTmaSlot + kPTX * kTY) * sizeof(double) + 64 + 128;
-constexpr size_t kTmaEvalSmem = (size_t)kTmaRing * kTmaSlot * sizeof(double) + 64 + 128;  // no rhs ring
+constexpr size_t kTmaSmem = (size_t)kTmaRing * (kTmaSlot + kPTX * kTY) * sizeof(double) + 128 + 128;
+constexpr size_t kTmaEvalSmem = (size_t)kTmaRing * kTmaSlot * sizeof(double) + 128 + 128;  // no rhs ring
 
 // The tensor maps one walk needs: x with the three box shapes, and the rhs (interior box).
 struct TmaMaps {
@@ -55,6 +56,9 @@ __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
 }
 __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
@@ -98,9 +102,17 @@ __device__ __forceinline__ void lds2(unsigned addr, double& a, double& b) {
 // inside the unrolled body every ring slot, mbarrier and phase parity is a compile-time constant:
 // plane k0 - 2 + j lives in slot j % 6 and is that slot's (j / 6)-th fill.  Staging distance 4:
 // the step of plane k waits for plane k + 2 and stages plane k + 4 into the slot of plane k - 2.
-template <bool HAS_AUX, class PlaneFn, class Body>
+//
+// FREE: no block barrier in the plane loop.  Slot reuse is then gated by a second mbarrier per slot
+// ("empty", one arrival per warp after the warp's last read of the slot: its x/y taps and rhs pair of
+// that plane; the two z-tap-only planes below the chunk are released after the prologue); the staging
+// lane waits for the empty phase of the slot it refills -- the plane two steps back, so warps drift up
+// to two planes apart and their FP64 bursts stop being phase-locked.  Measured on C5 (r3a, same box,
+// alternating runs): F_A/F_D 103.0 -> 96.1 ms per step (on), multigrid sweeps 125.8 -> 133.8 (off).
+template <bool HAS_AUX, bool FREE, class PlaneFn, class Body>
 __device__ __forceinline__ void walk_pair_tma(const TmaMaps& maps, int nx, int ny, int nz, const ZChunk& z,
                                               double* smem, PlaneFn plane, Body body) {
+  constexpr bool free_run = FREE;
   static_assert(kTmaRing == 6, "the unrolled walker is written for a 6-slot ring");
   constexpr int kSlotB = kTmaSlot * 8, kAuxB = kPTX * kTY * 8;
   const int i0 = blockIdx.x * kPTX, j0 = blockIdx.y * kTY;
@@ -120,16 +132,22 @@ __device__ __forceinline__ void walk_pair_tma(const TmaMaps& maps, int nx, int n
   const int ir = i0 + kPTX >= nx ? i0 + kPTX - nx : i0 + kPTX;  // columns 64, 65
   if (t == 0) {
 #pragma unroll
-    for (int r = 0; r < kTmaRing; ++r) mbar_init(bars + 8u * r, 1);
+    for (int r = 0; r < kTmaRing; ++r) {
+      mbar_init(bars + 8u * r, 1);
+      mbar_init(bars + 8u * (kTmaRing + r), kTY);  // "empty": one arrival per warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   // stage plane kk into slot R (compile-time)
-  auto issue = [&](auto slot, int kk) {
+  // refill: the slot held an earlier plane; in free-run mode wait until every warp released it
+  // (completion `empty_par` of the slot's empty barrier)
+  auto issue = [&](auto slot, int kk, bool refill = false, unsigned empty_par = 0u) {
     constexpr int R = decltype(slot)::value;
     if (ty != 0 || kk > z.k1 + 1) return;  // warp 0 stages (a warp is one tile row)
     if (!elect_one()) return;
     const unsigned bar = bars + 8u * R;
+    if (free_run && refill) mbar_wait(bars + 8u * (kTmaRing + R), empty_par);
     const bool aux = HAS_AUX && kk >= z.k0 && kk < z.k1;
     mbar_expect_tx(bar, kTmaPlaneBytes + (aux ? kTmaAuxBytes : 0u));
     const int zz = zoff + wrapi(kk, nz);
@@ -162,14 +180,21 @@ __device__ __forceinline__ void walk_pair_tma(const TmaMaps& maps, int nx, int n
   lds2<1 * kSlotB + kCtr>(ay0, q[0][1], q[1][1]);
   lds2<2 * kSlotB + kCtr>(ay0, q[0][2], q[1][2]);
   lds2<3 * kSlotB + kCtr>(ay0, q[0][3], q[1][3]);
+  if (free_run) {  // planes k0-2 and k0-1 are z taps only: their slots are released here
+    __syncwarp();
+    if (tx == 0) {
+      mbar_arrive(bars + 8u * (kTmaRing + 0));
+      mbar_arrive(bars + 8u * (kTmaRing + 1));
+    }
+  }
   // phase P of iteration it handles plane k = k0 + 6 it + P = fill it of slot (P + 2) % 6
   auto step = [&](auto ph, int k, unsigned par) {
     constexpr int P = decltype(ph)::value;
     constexpr int SK = (P + 2) % 6;   // slot of plane k
     constexpr int S2 = (P + 4) % 6;   // slot of plane k + 2: fill it + (P >= 2)
     mbar_wait(bars + 8u * S2, par ^ (P >= 2 ? 1u : 0u));  // plane k+2 has landed
-    __syncthreads();  // every thread is past plane k-1: the slot of plane k-2 is free
-    issue(Phase<P>{}, k + 4);
+    if (!free_run) __syncthreads();  // every thread is past plane k-1: the slot of plane k-2 is free
+    issue(Phase<P>{}, k + 4, true, par);  // slot P: its fill (it + 1) follows release number it
     lds2<S2 * kSlotB + kCtr>(ay0, q[0][(P + 4) % 6], q[1][(P + 4) % 6]);
     plane(k);
     PairTaps v;
@@ -189,6 +214,10 @@ __device__ __forceinline__ void walk_pair_tma(const TmaMaps& maps, int nx, int n
     }
     double av[2] = {0.0, 0.0};
     if (HAS_AUX) lds2<SK * kAuxB>(aa, av[0], av[1]);
+    if (free_run) {  // this warp's last read of plane k's slot
+      __syncwarp();
+      if (tx == 0) mbar_arrive(bars + 8u * (kTmaRing + SK));
+    }
     body(k, (unsigned)k * pl + col, v, av, true);
   };
   unsigned par = 0;
@@ -225,7 +254,7 @@ __global__ void __launch_bounds__(kTX* kTY, UCONST ? 3 : 2) k_eval_ad3_tma(Ops o
   for (int a = 0; a < 3; ++a) cd[a] = o.cdiff[s][a];
   AdvPair<UCONST> ad;
   ad.init(o, g);
-  walk_pair_tma<false>(
+  walk_pair_tma<false, true>(
       maps, g.nx, g.ny, g.nz, z, ev_tring, [&](int k) { ad.plane(g, k); },
       [&](int k, unsigned cell, const PairTaps& v, const double (&)[2], bool) {
         if (fas) {
