@@ -70,6 +70,22 @@ def test_engine_equals_reference_integrate_scaled_c5(gpu, eng, scheme, workers):
     assert np.allclose(gi, ri, rtol=1e-12, atol=0)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["c2", "c5"])
+def test_engine_equals_reference_imexq_adr(gpu, eng, name):
+    """IMEXQ on the periodic class with its coupled stage (cisdc_gpu.h): the compiled C++ side runs the
+    unmodified cisdc::integrate(Scheme::imexq) over AdrProblem::solve_coupled and Engine::integrate on
+    the same descriptor; states bit-identical, reports (sweeps, coupled solves) equal."""
+    import dataclasses
+    spec = P.config_c2(scale=128, n_steps=1) if name == "c2" else P.config_c5(scale=16)
+    prob = dataclasses.replace(spec.problem, coupled_tol=1e-13, coupled_max_iter=60)
+    o = api.IntegrateOptions(scheme=3, dt=spec.dt, n_steps=1, M=3, n_sweeps=2, nu=1)
+    g, r, gc, rc, gi, ri = run_both(eng, prob, spec.phi0, o, 0)
+    assert np.array_equal(g, r)
+    assert np.array_equal(gc, rc) and gc[3] == 6  # 3 nodes x 2 sweeps coupled solves
+    assert np.allclose(gi, ri, rtol=1e-12, atol=0)
+
+
 def exceptions(eng, desc, phi0, o, workers=0):
     c, oc = desc.to_c(), o.to_c()
     phi0 = np.ascontiguousarray(phi0, dtype=np.float64)
